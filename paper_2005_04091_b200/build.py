@@ -1,0 +1,60 @@
+"""Build libspconv.so (all CUDA sources, sm_100a) in-tree with nvcc."""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libspconv.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+         "--expt-relaxed-constexpr", "-Xcompiler", "-Wall"]
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = (sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.inc"))
+            + glob.glob(os.path.join(INCLUDE, "*.h")))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def generate() -> None:
+    """Regenerate the inline-PTX dispatcher include when its generator changed."""
+    inc = os.path.join(CSRC, "dispatch_gen.inc")
+    gen = os.path.join(CSRC, "gen_dispatch.py")
+    if not os.path.exists(inc) or os.path.getmtime(inc) < os.path.getmtime(gen):
+        subprocess.check_call([sys.executable, gen, inc])
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    generate()
+    if not force and not _stale():
+        return LIB
+    tmp = LIB + f".tmp{os.getpid()}"
+    cmd = [NVCC, *ARCH, *FLAGS, "-I", INCLUDE, "-I", CSRC, *sources(), "-o", tmp]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libspconv.so")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+        f.write(r.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,434 @@
+// spconv_api.cu — the C-ABI of include/spconv.h: plan creation (validate,
+// decode, group, upload), argument checking and the
+// kernel launches (a4-a6).  No CPU compute path exists: every output value is
+// produced by a CUDA kernel (kernel_generic.cu / kernel_tiled.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <numeric>
+#include <vector>
+
+#include "spconv_internal.h"
+
+using spconv::Plan;
+
+namespace {
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Host copy of an array that may live in host or device memory.
+template <typename T>
+int fetch(const T *src, int64_t n, std::vector<T> &dst) {
+    dst.resize(size_t(n));
+    if (n == 0) return SPCONV_OK;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, src);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        at.type = cudaMemoryTypeUnregistered;
+    }
+    if (at.type == cudaMemoryTypeDevice) {
+        if (cudaMemcpy(dst.data(), src, sizeof(T) * size_t(n), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return SPCONV_ERR_CUDA;
+    } else {
+        std::memcpy(dst.data(), src, sizeof(T) * size_t(n));
+    }
+    return SPCONV_OK;
+}
+
+template <typename T>
+int upload(T **dptr, const T *src, size_t n, int64_t &bytes) {
+    const size_t sz = sizeof(T) * std::max<size_t>(n, 1);
+    if (cudaMalloc(reinterpret_cast<void **>(dptr), sz) != cudaSuccess) {
+        cudaGetLastError();
+        return SPCONV_ERR_OOM;
+    }
+    bytes += int64_t(sz);
+    if (n && cudaMemcpy(*dptr, src, sizeof(T) * n, cudaMemcpyHostToDevice) != cudaSuccess)
+        return SPCONV_ERR_CUDA;
+    return SPCONV_OK;
+}
+
+void free_plan(Plan *p) {
+    if (!p) return;
+    DeviceGuard g(p->device);
+    cudaFree(p->d_rowptr);
+    cudaFree(p->d_taps);
+    cudaFree(p->d_values);
+    cudaFree(p->d_bias);
+    cudaFree(p->d_group_rows);
+    cudaFree(p->d_segoff);
+    cudaFree(p->d_stream);
+    cudaFree(p->d_xbuf);
+    cudaFree(p->d_ybuf);
+    cudaFree(p->d_abuf);
+    if (p->host_stream) cudaStreamDestroy(p->host_stream);
+    delete static_cast<spconv_plan_s *>(p);
+}
+
+// x/y/argmax must be device memory of the plan's device (no CPU fallback).
+int check_device_ptr(const void *ptr, int device) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return SPCONV_ERR_DEVICE;
+    }
+    if (at.type == cudaMemoryTypeManaged) return SPCONV_OK;
+    if (at.type != cudaMemoryTypeDevice || at.device != device) return SPCONV_ERR_DEVICE;
+    return SPCONV_OK;
+}
+
+bool overlap(const void *a, size_t abytes, const void *b, size_t bbytes) {
+    const char *a0 = static_cast<const char *>(a), *b0 = static_cast<const char *>(b);
+    return a0 < b0 + bbytes && b0 < a0 + abytes;
+}
+
+// Row groups with balanced nnz: longest-processing-time-first into
+// ceil(F/R) groups of at most R rows.
+std::vector<int32_t> balance_groups(const std::vector<int32_t> &rowptr, int F, int R, int &ngroups) {
+    ngroups = (F + R - 1) / R;
+    std::vector<int> order(F);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return rowptr[a + 1] - rowptr[a] > rowptr[b + 1] - rowptr[b];
+    });
+    std::vector<int64_t> load(ngroups, 0);
+    std::vector<int> fill(ngroups, 0);
+    std::vector<int32_t> rows(size_t(ngroups) * R, -1);
+    for (int f : order) {
+        int best = -1;
+        for (int g = 0; g < ngroups; ++g)
+            if (fill[g] < R && (best < 0 || load[g] < load[best])) best = g;
+        rows[size_t(best) * R + fill[best]++] = f;
+        load[best] += rowptr[f + 1] - rowptr[f];
+    }
+    return rows;
+}
+
+int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<int32_t> &colidx,
+               const std::vector<float> &values, const std::vector<float> &bias, int rows_per_group) {
+    const int K = p->K;
+    // a2: decode colidx -> (c, ky, kx)
+    std::vector<uint32_t> taps(size_t(p->nnz));
+    p->h_c.resize(size_t(p->nnz));
+    p->h_dy.resize(size_t(p->nnz));
+    p->h_dx.resize(size_t(p->nnz));
+    for (int64_t j = 0; j < p->nnz; ++j) {
+        const int col = colidx[size_t(j)];
+        const int c = col / (K * K), ky = (col / K) % K, kx = col % K;
+        taps[size_t(j)] = spconv::pack_tap(c, ky, kx);
+        p->h_c[size_t(j)] = c;
+        p->h_dy[size_t(j)] = ky - p->pad;
+        p->h_dx[size_t(j)] = kx - p->pad;
+    }
+    int st;
+    if ((st = upload(&p->d_rowptr, rowptr.data(), rowptr.size(), p->device_bytes))) return st;
+    if ((st = upload(&p->d_taps, taps.data(), taps.size(), p->device_bytes))) return st;
+    if ((st = upload(&p->d_values, values.data(), values.size(), p->device_bytes))) return st;
+    if ((st = upload(&p->d_bias, bias.data(), bias.size(), p->device_bytes))) return st;
+
+    if (p->kernel != SPCONV_KERNEL_TILED) return SPCONV_OK;
+    // a3: balanced row groups and the per-(group, channel) tap streams
+    const int R = rows_per_group;
+    p->R = R;
+    std::vector<int32_t> grows = balance_groups(rowptr, p->F, R, p->num_groups);
+    const int C = p->C;
+    std::vector<int32_t> segoff(size_t(p->num_groups) * (C + 1));
+    std::vector<spconv::TapEntry> stream;
+    stream.reserve(size_t(p->nnz) + size_t(p->num_groups) * C);
+    std::vector<std::vector<spconv::TapEntry>> bucket(C);
+    for (int g = 0; g < p->num_groups; ++g) {
+        for (auto &b : bucket) b.clear();
+        for (int r = 0; r < R; ++r) {
+            const int f = grows[size_t(g) * R + r];
+            if (f < 0) continue;
+            for (int32_t j = rowptr[f]; j < rowptr[f + 1]; ++j) {
+                const int col = colidx[size_t(j)];
+                const int c = col / 9, ky = (col / 3) % 3, kx = col % 3;
+                bucket[c].push_back({values[size_t(j)], r * 9 + ky * 3 + kx});
+            }
+        }
+        for (int c = 0; c < C; ++c) {
+            segoff[size_t(g) * (C + 1) + c] = int32_t(stream.size());
+            auto &b = bucket[c];
+            std::stable_sort(b.begin(), b.end(),
+                             [](const spconv::TapEntry &a, const spconv::TapEntry &b) { return a.id < b.id; });
+            stream.insert(stream.end(), b.begin(), b.end());
+            stream.push_back({0.0f, R * 9}); // sentinel: ends the channel's dispatch
+        }
+        segoff[size_t(g) * (C + 1) + C] = int32_t(stream.size());
+    }
+    if ((st = upload(&p->d_group_rows, grows.data(), grows.size(), p->device_bytes))) return st;
+    if ((st = upload(&p->d_segoff, segoff.data(), segoff.size(), p->device_bytes))) return st;
+    if ((st = upload(&p->d_stream, stream.data(), stream.size(), p->device_bytes))) return st;
+    spconv::tiled_geometry(*p);
+    return SPCONV_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+const char *spconv_status_string(int status) {
+    switch (status) {
+        case SPCONV_OK: return "ok";
+        case SPCONV_ERR_NULLPTR: return "required pointer is NULL";
+        case SPCONV_ERR_SHAPE: return "invalid shape";
+        case SPCONV_ERR_CSR: return "malformed CSR (rowptr/colidx/values)";
+        case SPCONV_ERR_UNSUPPORTED: return "unsupported shape or option";
+        case SPCONV_ERR_ALIGN: return "pointer not 4-byte aligned";
+        case SPCONV_ERR_DEVICE: return "pointer is not device memory of the plan's device";
+        case SPCONV_ERR_CUDA: return "CUDA error";
+        case SPCONV_ERR_OOM: return "out of memory";
+        case SPCONV_ERR_ALIAS: return "output overlaps input";
+        default: return "unknown status";
+    }
+}
+
+int spconv_abi_version(void) { return SPCONV_ABI_VERSION; }
+
+int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int stride, int pad,
+                     const int32_t *rowptr, const int32_t *colidx, const float *values, int64_t nnz,
+                     const float *bias, int device, const spconv_options_t *opts) {
+    if (!plan) return SPCONV_ERR_NULLPTR;
+    *plan = nullptr;
+    if (!rowptr || (nnz > 0 && (!colidx || !values))) return SPCONV_ERR_NULLPTR;
+    if (C < 1 || H < 1 || W < 1 || F < 1 || K < 1 || stride < 1 || pad < 0 || nnz < 0)
+        return SPCONV_ERR_SHAPE;
+    if (K > 8 || stride > 8 || pad > 16 || nnz > INT32_MAX || int64_t(C) * K * K > INT32_MAX / 2)
+        return SPCONV_ERR_UNSUPPORTED;
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    if (Hp < K || Wp < K) return SPCONV_ERR_SHAPE;
+    spconv_options_t o{};
+    if (opts) o = *opts;
+    if (o.kernel < SPCONV_KERNEL_AUTO || o.kernel > SPCONV_KERNEL_TILED) return SPCONV_ERR_UNSUPPORTED;
+    for (int r : o.reserved)
+        if (r != 0) return SPCONV_ERR_UNSUPPORTED;
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+        cudaGetLastError();
+        return SPCONV_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) return SPCONV_ERR_DEVICE;
+    DeviceGuard guard(device);
+    if (!guard.ok) return SPCONV_ERR_CUDA;
+
+    // a1: validate (host copies; inputs may be host or device pointers)
+    std::vector<int32_t> h_rowptr, h_colidx;
+    std::vector<float> h_values, h_bias;
+    int st;
+    if ((st = fetch(rowptr, F + 1, h_rowptr))) return st;
+    if ((st = fetch(colidx, nnz, h_colidx))) return st;
+    if ((st = fetch(values, nnz, h_values))) return st;
+    if (bias) {
+        if ((st = fetch(bias, F, h_bias))) return st;
+    } else {
+        h_bias.assign(size_t(F), 0.0f);
+    }
+    if (h_rowptr[0] != 0 || int64_t(h_rowptr[size_t(F)]) != nnz) return SPCONV_ERR_CSR;
+    const int32_t ncol = C * K * K;
+    for (int f = 0; f < F; ++f) {
+        const int32_t b = h_rowptr[size_t(f)], e = h_rowptr[size_t(f) + 1];
+        if (e < b) return SPCONV_ERR_CSR;
+        for (int32_t j = b; j < e; ++j) {
+            const int32_t col = h_colidx[size_t(j)];
+            if (col < 0 || col >= ncol) return SPCONV_ERR_CSR;
+            if (j > b && col <= h_colidx[size_t(j) - 1]) return SPCONV_ERR_CSR; // sorted, unique
+            if (!std::isfinite(h_values[size_t(j)])) return SPCONV_ERR_CSR;
+        }
+    }
+    for (float b : h_bias)
+        if (!std::isfinite(b)) return SPCONV_ERR_CSR;
+
+    spconv_plan_s *p = new (std::nothrow) spconv_plan_s;
+    if (!p) return SPCONV_ERR_OOM;
+    p->C = C; p->H = H; p->W = W; p->F = F; p->K = K; p->stride = stride; p->pad = pad;
+    p->Ho = (Hp - K) / stride + 1;
+    p->Wo = (Wp - K) / stride + 1;
+    p->nnz = nnz;
+    p->device = device;
+    const bool tiled_ok = spconv::tiled_supported(C, H, W, F, K, stride, pad);
+    if (o.kernel == SPCONV_KERNEL_TILED && !tiled_ok) {
+        delete p;
+        return SPCONV_ERR_UNSUPPORTED;
+    }
+    p->kernel = (o.kernel == SPCONV_KERNEL_GENERIC || !tiled_ok) ? SPCONV_KERNEL_GENERIC
+                                                                : SPCONV_KERNEL_TILED;
+    int R = o.rows_per_group;
+    if (R == 0) R = spconv::tiled_default_R(C, F, double(nnz) / (double(F) * ncol));
+    if (p->kernel == SPCONV_KERNEL_TILED && R != 4 && R != 8) {
+        delete p;
+        return SPCONV_ERR_UNSUPPORTED;
+    }
+    st = build_plan(p, h_rowptr, h_colidx, h_values, h_bias, R);
+    if (st) {
+        free_plan(p);
+        return st;
+    }
+    *plan = p;
+    return SPCONV_OK;
+}
+
+int spconv_create(spconv_plan_t *plan, int C, int H, int W, int F, int K, int stride, int pad,
+                  const int32_t *rowptr, const int32_t *colidx, const float *values, int64_t nnz,
+                  const float *bias, int device) {
+    return spconv_create_ex(plan, C, H, W, F, K, stride, pad, rowptr, colidx, values, nnz, bias,
+                            device, nullptr);
+}
+
+static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax, bool fused,
+               void *stream) {
+    if (!plan) return SPCONV_ERR_NULLPTR;
+    Plan *p = plan;
+    if (N < 0) return SPCONV_ERR_SHAPE;
+    if (fused && (p->Ho < 2 || p->Wo < 2)) return SPCONV_ERR_SHAPE;
+    if (N == 0) return SPCONV_OK;
+    if (!x || !y) return SPCONV_ERR_NULLPTR;
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+         reinterpret_cast<uintptr_t>(argmax)) & 3)
+        return SPCONV_ERR_ALIGN;
+    const size_t xbytes = size_t(N) * p->C * p->H * p->W * 4;
+    const size_t ybytes = fused ? size_t(N) * p->F * (p->Ho / 2) * (p->Wo / 2) * 4
+                                : size_t(N) * p->F * p->Ho * p->Wo * 4;
+    if (overlap(x, xbytes, y, ybytes)) return SPCONV_ERR_ALIAS;
+    if (argmax && (overlap(x, xbytes, argmax, ybytes) || overlap(y, ybytes, argmax, ybytes)))
+        return SPCONV_ERR_ALIAS;
+    int st;
+    if ((st = check_device_ptr(x, p->device)) || (st = check_device_ptr(y, p->device))) return st;
+    if (argmax && (st = check_device_ptr(argmax, p->device))) return st;
+    DeviceGuard guard(p->device);
+    if (!guard.ok) return SPCONV_ERR_CUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (p->kernel == SPCONV_KERNEL_TILED)
+        e = spconv::launch_tiled(*p, N, x, y, argmax, fused, s);
+    else
+        e = fused ? spconv::launch_generic_fused(*p, N, x, y, argmax, s)
+                  : spconv::launch_generic_conv(*p, N, x, y, s);
+    return e == cudaSuccess ? SPCONV_OK : SPCONV_ERR_CUDA;
+}
+
+int spconv_forward(spconv_plan_t plan, int N, const float *x, float *y, void *stream) {
+    return run(plan, N, x, y, nullptr, false, stream);
+}
+
+int spconv_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax,
+                              void *stream) {
+    return run(plan, N, x, y, argmax, true, stream);
+}
+
+int spconv_forward_host(spconv_plan_t plan, int N, const float *x_host, float *y_host, int fused,
+                        int32_t *argmax_host) {
+    if (!plan) return SPCONV_ERR_NULLPTR;
+    Plan *p = plan;
+    if (N < 0) return SPCONV_ERR_SHAPE;
+    if (fused && (p->Ho < 2 || p->Wo < 2)) return SPCONV_ERR_SHAPE;
+    if (N == 0) return SPCONV_OK;
+    if (!x_host || !y_host) return SPCONV_ERR_NULLPTR;
+    const size_t xn = size_t(N) * p->C * p->H * p->W;
+    const size_t yn = fused ? size_t(N) * p->F * (p->Ho / 2) * (p->Wo / 2)
+                            : size_t(N) * p->F * p->Ho * p->Wo;
+    std::lock_guard<std::mutex> lock(p->host_mu);
+    DeviceGuard guard(p->device);
+    if (!guard.ok) return SPCONV_ERR_CUDA;
+    if (!p->host_stream && cudaStreamCreateWithFlags(&p->host_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return SPCONV_ERR_CUDA;
+    if (xn > p->xbuf_elems) {
+        cudaFree(p->d_xbuf);
+        p->d_xbuf = nullptr;
+        p->xbuf_elems = 0;
+        if (cudaMalloc(&p->d_xbuf, xn * 4) != cudaSuccess) { cudaGetLastError(); return SPCONV_ERR_OOM; }
+        p->xbuf_elems = xn;
+    }
+    if (yn > p->ybuf_elems) {
+        cudaFree(p->d_ybuf);
+        cudaFree(p->d_abuf);
+        p->d_ybuf = nullptr;
+        p->d_abuf = nullptr;
+        p->ybuf_elems = 0;
+        if (cudaMalloc(&p->d_ybuf, yn * 4) != cudaSuccess || cudaMalloc(&p->d_abuf, yn * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return SPCONV_ERR_OOM;
+        }
+        p->ybuf_elems = yn;
+    }
+    cudaStream_t s = p->host_stream;
+    if (cudaMemcpyAsync(p->d_xbuf, x_host, xn * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return SPCONV_ERR_CUDA;
+    int32_t *dam = (fused && argmax_host) ? p->d_abuf : nullptr;
+    int st = run(plan, N, p->d_xbuf, p->d_ybuf, dam, fused != 0, s);
+    if (st) return st;
+    if (cudaMemcpyAsync(y_host, p->d_ybuf, yn * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return SPCONV_ERR_CUDA;
+    if (dam && cudaMemcpyAsync(argmax_host, dam, yn * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return SPCONV_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return SPCONV_ERR_CUDA;
+    return SPCONV_OK;
+}
+
+int spconv_destroy(spconv_plan_t plan) {
+    free_plan(plan);
+    return SPCONV_OK;
+}
+
+int spconv_output_dims(spconv_plan_t plan, int N, int fused, int64_t dims[4]) {
+    if (!plan || !dims) return SPCONV_ERR_NULLPTR;
+    if (N < 0) return SPCONV_ERR_SHAPE;
+    dims[0] = N;
+    dims[1] = plan->F;
+    dims[2] = fused ? plan->Ho / 2 : plan->Ho;
+    dims[3] = fused ? plan->Wo / 2 : plan->Wo;
+    return SPCONV_OK;
+}
+
+int spconv_plan_info(spconv_plan_t plan, spconv_plan_info_t *info) {
+    if (!plan || !info) return SPCONV_ERR_NULLPTR;
+    const Plan *p = plan;
+    std::memset(info, 0, sizeof(*info));
+    info->C = p->C; info->H = p->H; info->W = p->W; info->F = p->F; info->K = p->K;
+    info->stride = p->stride; info->pad = p->pad; info->Ho = p->Ho; info->Wo = p->Wo;
+    info->nnz = p->nnz;
+    info->device = p->device;
+    info->kernel = p->kernel;
+    info->rows_per_group = p->R;
+    info->num_groups = p->num_groups;
+    info->device_bytes = p->device_bytes;
+    info->launches_per_call = 1;
+    return SPCONV_OK;
+}
+
+int spconv_debug_decoded(spconv_plan_t plan, int32_t *c, int32_t *dy, int32_t *dx) {
+    if (!plan) return SPCONV_ERR_NULLPTR;
+    const Plan *p = plan;
+    if (p->nnz > 0 && (!c || !dy || !dx)) return SPCONV_ERR_NULLPTR;
+    // Read back what was uploaded to the device, so the check covers the device copy.
+    std::vector<uint32_t> taps(size_t(p->nnz));
+    if (p->nnz) {
+        DeviceGuard guard(p->device);
+        if (cudaMemcpy(taps.data(), p->d_taps, taps.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return SPCONV_ERR_CUDA;
+    }
+    for (int64_t j = 0; j < p->nnz; ++j) {
+        const uint32_t t = taps[size_t(j)];
+        c[j] = int32_t(t >> 6);
+        dy[j] = int32_t((t >> 3) & 7u) - p->pad;
+        dx[j] = int32_t(t & 7u) - p->pad;
+    }
+    return SPCONV_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,84 @@
+// spconv_internal.h — plan layout shared by the C-ABI (spconv_api.cu) and the
+// kernels (kernel_generic.cu, kernel_tiled.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <vector>
+
+#include "spconv.h"
+
+namespace spconv {
+
+// Packed decoded tap for the generic kernel:
+// bits [31:6] = c, [5:3] = ky, [2:0] = kx  (K <= 8).
+__host__ __device__ inline uint32_t pack_tap(int c, int ky, int kx) {
+    return (uint32_t(c) << 6) | (uint32_t(ky) << 3) | uint32_t(kx);
+}
+
+// Tiled-kernel stream entry: one nonzero of a row group, in the order the
+// kernel consumes it (channel-major, then case id ascending).
+struct TapEntry {
+    float v;    // filter value (bit-exact copy of values[j])
+    int32_t id; // r * 9 + ky * 3 + kx  (r = slot of the output channel in its group); R*9 = end
+};
+
+struct TiledGeometry {
+    int R, T, S;        // rows per group, output rows / cols per thread tile
+    int tiles_x, tiles_y, tiles_per_img;
+    int blocks_per_img; // ceil(tiles_per_img / 32)
+    int rows_staged;    // RB: input rows staged per pixel block (max over blocks)
+    int pitch;          // smem words per staged input row (>= W + 2, multiple of 4)
+    int cc;             // channels per pipeline stage
+    int nstage;         // pipeline depth
+    int groups_per_cta; // GPC: one warp per group
+    int num_gsets;      // ceil(num_groups / GPC)
+    bool tma_ok;        // W * 4 % 16 == 0 (TMA global stride rule)
+    size_t smem_bytes;
+};
+
+struct Plan {
+    int C, H, W, F, K, stride, pad, Ho, Wo;
+    int64_t nnz;
+    int device;
+    int kernel; // SPCONV_KERNEL_GENERIC or SPCONV_KERNEL_TILED
+    // device copies (generic path)
+    int32_t *d_rowptr = nullptr;
+    uint32_t *d_taps = nullptr;
+    float *d_values = nullptr;
+    float *d_bias = nullptr; // always F floats (zeros when bias == NULL)
+    // host copies for spconv_debug_decoded
+    std::vector<int32_t> h_c, h_dy, h_dx;
+    // tiled path
+    int R = 0, num_groups = 0;
+    int32_t *d_group_rows = nullptr; // [num_groups * R], -1 = empty slot
+    int32_t *d_segoff = nullptr;     // [num_groups * (C + 1)] offsets into d_stream
+    TapEntry *d_stream = nullptr;    // [nnz + num_groups*C]: per (group, channel) taps + sentinel
+    TiledGeometry geo{};
+    int64_t device_bytes = 0;
+    // spconv_forward_host staging
+    std::mutex host_mu;
+    float *d_xbuf = nullptr, *d_ybuf = nullptr;
+    int32_t *d_abuf = nullptr;
+    size_t xbuf_elems = 0, ybuf_elems = 0;
+    cudaStream_t host_stream = nullptr;
+};
+
+// kernel_generic.cu
+cudaError_t launch_generic_conv(const Plan &p, int N, const float *x, float *y, cudaStream_t s);
+cudaError_t launch_generic_fused(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
+                                 cudaStream_t s);
+
+// kernel_tiled.cu
+bool tiled_supported(int C, int H, int W, int F, int K, int stride, int pad);
+int tiled_default_R(int C, int F, double density);
+void tiled_geometry(Plan &p); // fills p.geo for p.R
+cudaError_t launch_tiled(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
+                         bool fused, cudaStream_t s);
+
+} // namespace spconv
+
+// The opaque handle type of the public ABI is the plan itself.
+struct spconv_plan_s : public spconv::Plan {};

@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar: bitwise equality with the FP32-ordered oracle for
+conv values, pooled values, argmax indices and decode (reading G7 makes the
+kernel's accumulation order the oracle's); plus the north_star tolerance
+|g - o| <= 1e-4 + 1e-5 |o| against the FP64 oracle.  Small batches are compared
+element by element; full BASELINE.json sizes in the bench launch
+configuration are compared on sampled outputs the oracle computes one by one.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+from tests._util import allclose_contract, bits
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+KERNELS = ["tiled", "generic"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build_library()
+
+
+def _layer(cfg, csr, bias, kernel):
+    from paper_2005_04091_b200 import SparseConv2d
+    return SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, cfg.K, cfg.stride, cfg.pad, csr.rowptr,
+                        csr.colidx, csr.values, bias, device=0, kernel=kernel)
+
+
+def _bias(cfg):
+    return synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3))
+
+
+def _check_full(cfg, kernel, fused, N=None, integer=False):
+    if N is not None:
+        cfg = cfg.with_batch(N)
+    L = synthgen.make_layer(cfg, integer=integer)
+    c = L.csr
+    b = synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3), integer=integer)
+    layer = _layer(cfg, c, b, kernel)
+    x = torch.from_numpy(L.x).cuda()
+    args = (L.x, cfg.F, cfg.K, cfg.stride, cfg.pad, c.rowptr, c.colidx, c.values, b)
+    if not fused:
+        y = layer(x).cpu().numpy()
+        ref = oracle.conv_f32(*args)
+        assert y.shape == ref.shape
+        mism = np.count_nonzero(bits(y) != bits(ref))
+        assert mism == 0, f"{mism} of {y.size} outputs differ bitwise"
+        ok, worst = allclose_contract(y, oracle.conv_f64(*args))
+        assert ok, worst
+    else:
+        p, am = layer.fused_relu_maxpool(x)
+        p, am = p.cpu().numpy(), am.cpu().numpy()
+        rp, ra = oracle.fused_f32(*args)
+        assert p.shape == rp.shape
+        assert np.array_equal(bits(p), bits(rp))
+        assert np.array_equal(am, ra)
+    layer.close()
+
+
+# ---------------------------------------------------------------- configs, element by element
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c1_full(kernel):
+    _check_full(synthgen.CONFIGS["c1"], kernel, fused=False)
+    _check_full(synthgen.CONFIGS["c1"], kernel, fused=True)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("name,fused", [("c2", False), ("c3", True), ("c3", False), ("c2", True)])
+def test_c2_c3_small_batch(kernel, name, fused):
+    _check_full(synthgen.CONFIGS[name], kernel, fused, N=2)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("name", ["c4_50", "c4_80", "c4_90", "c4_95"])
+def test_c4_small_batch(kernel, name):
+    _check_full(synthgen.CONFIGS[name], kernel, fused=False, N=2)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c5_one_image(kernel):
+    _check_full(synthgen.CONFIGS["c5"], kernel, fused=False, N=1)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_integer_mode_exact(kernel):
+    _check_full(synthgen.CONFIGS["c2"], kernel, fused=False, N=1, integer=True)
+    _check_full(synthgen.CONFIGS["c3"], kernel, fused=True, N=1, integer=True)
+
+
+# ---------------------------------------------------------------- full sizes, sampled
+def _sample_pts(shape, n, seed):
+    rng = np.random.default_rng(seed)
+    pts = np.stack([rng.integers(0, s, n) for s in shape], axis=1)
+    # always include the corners / borders of the first and last planes
+    extra = []
+    for nn in (0, shape[0] - 1):
+        for f in (0, shape[1] - 1):
+            for yy in (0, shape[2] - 1):
+                for xx in (0, shape[3] - 1):
+                    extra.append((nn, f, yy, xx))
+    return np.concatenate([pts, np.array(extra)], axis=0)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4_50", "c4_95", "c5"])
+def test_full_size_sampled(name):
+    cfg = synthgen.CONFIGS[name]
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    layer = _layer(cfg, c, b, "auto")
+    x = torch.from_numpy(L.x).cuda()
+    args = (L.x, cfg.F, cfg.K, cfg.stride, cfg.pad, c.rowptr, c.colidx, c.values, b)
+    if cfg.fused:
+        p, am = layer.fused_relu_maxpool(x)
+        p, am = p.cpu().numpy(), am.cpu().numpy()
+        pts = _sample_pts(p.shape, 3000, 1)
+        rv, ra = oracle.fused_points_f32(*args, pts)
+        idx = tuple(pts.T)
+        assert np.array_equal(bits(p[idx]), bits(rv))
+        assert np.array_equal(am[idx], ra)
+        # property at any size: pooled >= 0 and argmax inside its window
+        assert (p >= 0).all()
+        py = np.arange(p.shape[2])[None, None, :, None]
+        px = np.arange(p.shape[3])[None, None, None, :]
+        r, q = am // layer.Wo, am % layer.Wo
+        assert ((r - 2 * py >= 0) & (r - 2 * py <= 1) & (q - 2 * px >= 0) & (q - 2 * px <= 1)).all()
+    else:
+        y = layer(x).cpu().numpy()
+        pts = _sample_pts(y.shape, 3000, 2)
+        idx = tuple(pts.T)
+        rv = oracle.conv_points_f32(*args, pts)
+        assert np.array_equal(bits(y[idx]), bits(rv))
+        ok, worst = allclose_contract(y[idx], oracle.conv_points_f64(*args, pts))
+        assert ok, worst
+        assert np.isfinite(y).all()
+    layer.close()
+
+
+# ---------------------------------------------------------------- edge cases
+EDGE = [
+    # N, C, H, W, F, K, stride, pad, density, kernel
+    (1, 3, 5, 7, 4, 3, 1, 1, 0.4, "tiled"),      # ragged tiles, W % 4 != 0 -> cp.async staging
+    (3, 5, 13, 11, 9, 3, 1, 1, 0.3, "tiled"),    # F not a multiple of R, odd sizes
+    (2, 4, 1, 1, 3, 3, 1, 1, 0.5, "tiled"),      # 1x1 image
+    (2, 7, 9, 20, 5, 3, 1, 1, 1.0, "tiled"),     # 0% sparsity (dense)
+    (1, 17, 6, 40, 12, 3, 1, 1, 0.15, "tiled"),  # C not a multiple of the channel chunk
+    (2, 3, 9, 9, 4, 3, 2, 1, 0.5, "generic"),    # stride 2
+    (1, 2, 8, 6, 3, 5, 1, 2, 0.4, "generic"),    # K = 5
+    (2, 6, 7, 7, 5, 1, 1, 0, 0.5, "generic"),    # K = 1
+    (1, 3, 10, 9, 2, 7, 2, 3, 0.2, "generic"),   # K = 7, stride 2
+    (1, 4, 6, 6, 4, 3, 1, 0, 0.5, "generic"),    # valid conv (pad 0)
+    (1, 4, 6, 6, 4, 3, 1, 1, 0.0, "tiled"),      # nnz = 0 -> bias
+    (1, 4, 6, 6, 4, 3, 1, 1, 0.0, "generic"),
+]
+
+
+@pytest.mark.parametrize("case", EDGE)
+def test_edge_cases(case):
+    N, C, H, W, F, K, s, p, d, kernel = case
+    seed = 777 + EDGE.index(case) * 10
+    csr = synthgen.make_csr(F, C, K, d, seed, seed + 1)
+    xh = synthgen.make_input((N, C, H, W), seed + 2)
+    b = synthgen.make_bias(F, seed + 3)
+    from paper_2005_04091_b200 import SparseConv2d
+    layer = SparseConv2d(C, H, W, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b, kernel=kernel)
+    assert layer.info["kernel"] == (2 if kernel == "tiled" else 1)
+    x = torch.from_numpy(xh).cuda()
+    y = layer(x).cpu().numpy()
+    ref = oracle.conv_f32(xh, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b)
+    assert np.array_equal(bits(y), bits(ref))
+    if layer.Ho >= 2 and layer.Wo >= 2:
+        pp, am = layer.fused_relu_maxpool(x)
+        rp, ra = oracle.fused_f32(xh, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b)
+        assert np.array_equal(bits(pp.cpu().numpy()), bits(rp))
+        assert np.array_equal(am.cpu().numpy(), ra)
+    layer.close()
+
+
+def test_unaligned_input_uses_cp_async_path():
+    cfg = synthgen.CONFIGS["c2"].with_batch(1)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    layer = _layer(cfg, c, None, "tiled")
+    buf = torch.empty(L.x.size + 1, dtype=torch.float32, device="cuda")
+    x = buf[1:].view(L.x.shape)  # 4-byte aligned, not 16-byte aligned
+    x.copy_(torch.from_numpy(L.x))
+    y = layer(x).cpu().numpy()
+    ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, None)
+    assert np.array_equal(bits(y), bits(ref))
+
+
+def test_batch_zero_is_noop_and_errors():
+    from paper_2005_04091_b200 import SparseConv2d, SpconvError, spconv
+    cfg = synthgen.CONFIGS["c1"]
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    layer = _layer(cfg, c, None, "auto")
+    y = torch.full((1, cfg.F, 16, 16), 7.0, device="cuda")
+    spconv.spconv_forward(layer.plan, 0, 0, 0)  # N = 0: no-op, NULL pointers allowed
+    x = torch.from_numpy(L.x).cuda()
+    # host pointer for x -> DEVICE error, nothing written
+    xh = torch.from_numpy(L.x)
+    with pytest.raises(SpconvError) as e:
+        spconv.spconv_forward(layer.plan, 1, xh.data_ptr(), y.data_ptr())
+    assert e.value.status == -6
+    assert (y == 7.0).all()
+    # aliasing
+    big = torch.zeros(L.x.size * 2, device="cuda")
+    with pytest.raises(SpconvError) as e:
+        spconv.spconv_forward(layer.plan, 1, big.data_ptr(), big.data_ptr() + 64)
+    assert e.value.status == -9
+    # misaligned
+    with pytest.raises(SpconvError) as e:
+        spconv.spconv_forward(layer.plan, 1, x.data_ptr() + 2, y.data_ptr())
+    assert e.value.status == -5
+    # malformed CSR is rejected at create (unsorted row)
+    bad = c.colidx.copy()
+    bad[0], bad[1] = bad[1], bad[0]
+    with pytest.raises(SpconvError) as e:
+        SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, bad, c.values)
+    assert e.value.status == -3
+    layer.close()
+
+
+def test_decode_bit_exact_vs_oracle():
+    cfg = synthgen.CONFIGS["c2"]
+    L = synthgen.make_layer(cfg, with_input=False)
+    c = L.csr
+    for kernel in KERNELS:
+        layer = _layer(cfg, c, None, kernel)
+        gc, gdy, gdx = layer.debug_decoded()
+        oc, oky, okx = oracle.decode(3, c.colidx)
+        assert np.array_equal(gc, oc) and np.array_equal(gdy, oky - 1) and np.array_equal(gdx, okx - 1)
+        layer.close()
+
+
+def test_csr_from_device_pointers():
+    cfg = synthgen.CONFIGS["c1"]
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    from paper_2005_04091_b200 import SparseConv2d
+    layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, torch.from_numpy(c.rowptr).cuda(),
+                         torch.from_numpy(c.colidx).cuda(), torch.from_numpy(c.values).cuda(),
+                         torch.from_numpy(b).cuda())
+    y = layer(torch.from_numpy(L.x).cuda()).cpu().numpy()
+    ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+    assert np.array_equal(bits(y), bits(ref))
+
+
+def test_forward_host_matches():
+    cfg = synthgen.CONFIGS["c3"].with_batch(2)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    layer = _layer(cfg, c, b, "auto")
+    y = layer.forward_host(L.x)
+    ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+    assert np.array_equal(bits(y), bits(ref))
+    p, am = layer.forward_host(L.x, fused=True)
+    rp, ra = oracle.fused_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+    assert np.array_equal(bits(p), bits(rp)) and np.array_equal(am, ra)
+
+
+# ---------------------------------------------------------------- GPU self-consistency
+def test_fused_equals_pool_of_forward_and_batch_independence():
+    cfg = synthgen.CONFIGS["c3"].with_batch(6)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    layer = _layer(cfg, c, b, "auto")
+    x = torch.from_numpy(L.x).cuda()
+    y = layer(x)
+    p, am = layer.fused_relu_maxpool(x)
+    rp, ra = torch.nn.functional.max_pool2d(torch.relu(y), 2, 2, return_indices=True)
+    assert torch.equal(p.view(torch.int32), rp.view(torch.int32))
+    assert torch.equal(am.long(), ra)
+    y3 = layer(x[3:4].contiguous())
+    assert torch.equal(y3.view(torch.int32), y[3:4].view(torch.int32))
+    y_again = layer(x)
+    assert torch.equal(y_again.view(torch.int32), y.view(torch.int32))
+
+
+def test_concurrent_streams():
+    cfg = synthgen.CONFIGS["c2"].with_batch(4)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    layer = _layer(cfg, c, None, "auto")
+    x = torch.from_numpy(L.x).cuda()
+    ref = layer(x)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    torch.cuda.synchronize()
+    for s in (s1, s2):
+        with torch.cuda.stream(s):
+            outs.append(layer(x))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.view(torch.int32), ref.view(torch.int32))
