@@ -141,6 +141,10 @@ const char *spconv_status_string(int status);
 
 int spconv_abi_version(void);
 
+/* Static description of the last CUDA runtime error an entry point of this
+ * library returned SPCONV_ERR_CUDA for on the calling thread (never NULL). */
+const char *spconv_last_cuda_error(void);
+
 /* Test-only: the decoded taps held by the plan, host outputs of nnz each:
  * c[j], dy[j] = ky_j - pad, dx[j] = kx_j - pad. */
 int spconv_debug_decoded(spconv_plan_t plan, int32_t *c, int32_t *dy, int32_t *dx);

@@ -282,16 +282,16 @@ template <int R, bool FUSED, bool TMA>
 cudaError_t launch_one(const CUtensorMap &map, const TiledArgs &a, int grid, size_t smem,
                        cudaStream_t s) {
     auto kern = tiled_kernel<R, FUSED, TMA>;
-    // Opt in to >48 KB dynamic shared memory once per (instantiation, device).
-    static unsigned long long attr_done = 0;
+    // Opt in to the dynamic shared memory this launch needs (the attribute must not
+    // exceed 227 KB minus the kernel's static shared memory); cached per device.
+    static size_t attr_done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    const unsigned long long bit = 1ull << (dev & 63);
-    if (!(__atomic_load_n(&attr_done, __ATOMIC_ACQUIRE) & bit)) {
-        cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    size_t &done = attr_done[dev & 63];
+    if (smem > 48 * 1024 && __atomic_load_n(&done, __ATOMIC_ACQUIRE) < smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
-        __atomic_fetch_or(&attr_done, bit, __ATOMIC_RELEASE);
+        __atomic_store_n(&done, smem, __ATOMIC_RELEASE);
     }
     kern<<<grid, 32 * a.gpc, smem, s>>>(map, a);
     return cudaGetLastError();
@@ -390,7 +390,9 @@ cudaError_t launch_tiled(const Plan &p, int N, const float *x, float *y, int32_t
 
     CUtensorMap map;
     memset(&map, 0, sizeof(map));
-    bool use_tma = g.tma_ok && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    // TMA tile loads need a 16-byte-aligned innermost start coordinate (probe:
+    // scripts/probes/tma_probe.cu); this kernel stages from ix = -1, so it uses cp.async.
+    bool use_tma = false && g.tma_ok && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     if (use_tma) {
         auto enc = get_encode();
         if (!enc) {

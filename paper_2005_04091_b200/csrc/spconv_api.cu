@@ -16,6 +16,14 @@ using spconv::Plan;
 
 namespace {
 
+// Last CUDA error seen by an entry point on this thread (spconv_last_cuda_error).
+thread_local cudaError_t g_last_cuda = cudaSuccess;
+
+int cuda_fail(cudaError_t e) {
+    g_last_cuda = e;
+    return SPCONV_ERR_CUDA;
+}
+
 // Restores the caller's current device on scope exit.
 struct DeviceGuard {
     int prev = -1;
@@ -200,6 +208,10 @@ const char *spconv_status_string(int status) {
 
 int spconv_abi_version(void) { return SPCONV_ABI_VERSION; }
 
+const char *spconv_last_cuda_error(void) {
+    return g_last_cuda == cudaSuccess ? "no CUDA error" : cudaGetErrorString(g_last_cuda);
+}
+
 int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int stride, int pad,
                      const int32_t *rowptr, const int32_t *colidx, const float *values, int64_t nnz,
                      const float *bias, int device, const spconv_options_t *opts) {
@@ -319,7 +331,7 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     else
         e = fused ? spconv::launch_generic_fused(*p, N, x, y, argmax, s)
                   : spconv::launch_generic_conv(*p, N, x, y, s);
-    return e == cudaSuccess ? SPCONV_OK : SPCONV_ERR_CUDA;
+    return e == cudaSuccess ? SPCONV_OK : cuda_fail(e);
 }
 
 int spconv_forward(spconv_plan_t plan, int N, const float *x, float *y, void *stream) {

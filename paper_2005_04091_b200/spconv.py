@@ -24,13 +24,17 @@ KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED
 # Every symbol include/spconv.h declares (checked by tests/test_abi.py).
 EXPORTS = ("spconv_create", "spconv_create_ex", "spconv_forward", "spconv_fused_relu_maxpool",
            "spconv_forward_host", "spconv_destroy", "spconv_output_dims", "spconv_plan_info",
-           "spconv_status_string", "spconv_abi_version", "spconv_debug_decoded")
+           "spconv_status_string", "spconv_abi_version", "spconv_debug_decoded",
+           "spconv_last_cuda_error")
 
 
 class SpconvError(RuntimeError):
     def __init__(self, status: int, what: str):
         self.status = status
-        super().__init__(f"{what}: {STATUS.get(status, status)} ({status_string(status)})")
+        msg = f"{what}: {STATUS.get(status, status)} ({status_string(status)})"
+        if status == -7 and _lib is not None:
+            msg += f": {_lib.spconv_last_cuda_error().decode()}"
+        super().__init__(msg)
 
 
 class Options(ctypes.Structure):
@@ -70,9 +74,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.spconv_status_string.argtypes = [I]
     lib.spconv_status_string.restype = ctypes.c_char_p
     lib.spconv_abi_version.argtypes = []
+    lib.spconv_last_cuda_error.argtypes = []
+    lib.spconv_last_cuda_error.restype = ctypes.c_char_p
     lib.spconv_debug_decoded.argtypes = [vp, vp, vp, vp]
     for name in EXPORTS:
-        if name not in ("spconv_status_string",):
+        if name not in ("spconv_status_string", "spconv_last_cuda_error"):
             getattr(lib, name).restype = I
     _lib = lib
     return lib
