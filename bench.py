@@ -219,7 +219,7 @@ def run_native(args, cfg):
     else:
         rp, ci, vv, b = L.csr.rowptr, L.csr.colidx, L.csr.values, L.bias
     layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, cfg.K, cfg.stride, cfg.pad, rp, ci, vv, b,
-                         device=local, kernel=args.kernel)
+                         device=local, kernel=args.kernel, rows_per_group=args.rows)
     torch.cuda.synchronize()
     create_ms = 1e3 * (time.perf_counter() - t0)
     info = layer.info
@@ -332,7 +332,8 @@ def run_native(args, cfg):
         "config": _config(cfg, world, f"rotating {nsets} input/output sets "
                                        f"({nsets * (in_bytes + out_bytes) / 2**20:.0f} MiB > 126 MiB L2)"),
         "images_per_s": round(images_per_s, 1),
-        "kernel": {1: "generic", 2: "tiled"}[info["kernel"]],
+        "kernel": {1: "generic", 2: "tiled", 3: "pipe"}[info["kernel"]],
+        "rows_per_group": int(info["rows_per_group"]),
         "kernel_ms": round(kern_ms, 5),
         "create_ms": round(create_ms, 3),
         "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
@@ -371,7 +372,7 @@ def _profiled_traffic(name, info):
         with open(path) as f:
             d = json.load(f)
         e = d.get(name)
-        if e and e.get("kernel") == {1: "generic", 2: "tiled"}[info["kernel"]]:
+        if e and e.get("kernel") == {1: "generic", 2: "tiled", 3: "pipe"}[info["kernel"]]:
             return e.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
@@ -385,7 +386,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c2", choices=sorted(synthgen.CONFIGS))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "tiled", "generic"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "pipe", "tiled", "generic"])
+    ap.add_argument("--rows", type=int, default=0, help="rows per group R (0 = library default)")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle CPU work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -66,13 +66,15 @@ enum {
     SPCONV_ERR_ALIAS = -9        /* y (or argmax) overlaps x                        */
 };
 
-/* Kernel selection (spconv_create_ex).  AUTO picks the register-tiled kernel
- * when the shape is supported by it (K = 3, stride 1, pad 1) and the generic
- * kernel otherwise.  Both are CUDA kernels; both obey the same contract. */
+/* Kernel selection (spconv_create_ex).  AUTO picks the pipelined kernel when
+ * the shape is supported by it (K = 3, stride 1, pad 1, Wo <= 125), else the
+ * register-tiled v1 kernel (K = 3, stride 1, pad 1), else the generic kernel.
+ * All are CUDA kernels; all obey the same arithmetic contract. */
 enum {
     SPCONV_KERNEL_AUTO = 0,
     SPCONV_KERNEL_GENERIC = 1,   /* one thread per output; any supported shape    */
-    SPCONV_KERNEL_TILED = 2      /* row-grouped register tiles, smem staging      */
+    SPCONV_KERNEL_TILED = 2,     /* v1: row-grouped register tiles, cp.async      */
+    SPCONV_KERNEL_PIPE = 3       /* v2: warp-specialised TMA pipeline, FFMA2      */
 };
 
 typedef struct spconv_plan_s *spconv_plan_t;

@@ -32,10 +32,11 @@ def _stale() -> bool:
 
 def generate() -> None:
     """Regenerate the inline-PTX dispatcher include when its generator changed."""
-    inc = os.path.join(CSRC, "dispatch_gen.inc")
-    gen = os.path.join(CSRC, "gen_dispatch.py")
-    if not os.path.exists(inc) or os.path.getmtime(inc) < os.path.getmtime(gen):
-        subprocess.check_call([sys.executable, gen, inc])
+    for inc_name, gen_name in (("dispatch_gen.inc", "gen_dispatch.py"), ("dispatch2_gen.inc", "gen_dispatch2.py")):
+        inc = os.path.join(CSRC, inc_name)
+        gen = os.path.join(CSRC, gen_name)
+        if not os.path.exists(inc) or os.path.getmtime(inc) < os.path.getmtime(gen):
+            subprocess.check_call([sys.executable, gen, inc])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

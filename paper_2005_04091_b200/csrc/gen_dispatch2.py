@@ -1,0 +1,137 @@
+"""Generate dispatch2_gen.inc: the tap dispatcher of kernel_pipe.cu (v2 kernel).
+
+For one (row group, pipeline stage of input channels) a warp walks a
+shared-memory stream of 16-byte entries {v, v, case, 0}.  Every tap
+case = r*9 + ky*3 + kx selects the FMAs of one CSR nonzero on the thread's
+T x S output tile ("out[n][y][x] +=
+coeff * in[...]"):
+
+    acc[r][t][s] = fma(v, x[t+ky][s+kx], acc[r][t][s])   t < T, s < S
+
+Accumulators and the (T+2) x (S+2) input window live in 64-bit register
+pairs so that the even-kx cases issue packed fma.rn.f32x2 (FFMA2: T*S/2
+instructions for T*S FMAs, per-component rounding identical to fmaf); kx = 1
+needs the odd pairs (x1,x2),(x3,x4),..., which are not register pairs, and
+issues T*S scalar FFMA.
+
+Dispatch is "threaded code" through one brx.idx jump table, software-
+pipelined one entry deep: the entry of nonzero k+1 is already in registers
+when case k starts, so the jump-table load for k+1 (an indexed constant
+load) is issued at the top of case k and overlaps its FMAs; case k also
+loads entry k+2.  Long case bodies (T*S FMAs) are what hide that latency
+(scripts/probes/dispatch_probe.cu measures it).
+
+One walk covers all channels of a pipeline stage: case R*9 ("next channel")
+advances the window pointer by one staged channel and reloads the window
+from shared memory, case R*9+1 ends the walk.
+
+Run: python gen_dispatch2.py [out]  (build.py runs it when the output is stale).
+"""
+import os
+import sys
+
+# (R, T, S) variants instantiated by kernel_pipe.cu
+VARIANTS = [(4, 4, 8)]
+
+
+def gen(R: int, T: int, S: int) -> str:
+    PAIRS = (S + 2) // 2  # window pairs per row
+    SH = S // 2           # accumulator pairs per output row
+    nacc = R * T * SH
+
+    def A(r, t, h):
+        return f"%{(r * T + t) * SH + h}"
+
+    XBASE = nacc + 1  # operand index of the first window pair (after the pointer output)
+
+    def X(i, j):
+        return f"%{XBASE + i * PAIRS + j}"
+
+    def tail():
+        return ["mov.b64 %%va, %%vb;",
+                "ld.shared.v2.b64 {%%vb, %%kb}, [%%sp];",  # entry k+2
+                "add.u32 %%sp, %%sp, 16;",
+                f"brx.idx.uni %%cn, $D{tag}_T;"]
+
+    P = f"%{nacc}"  # u32 shared-memory stream address, in/out
+    WP = f"%{nacc + 1 + (T + 2) * PAIRS}"  # u32 window address (in/out)
+    CHS = f"%{nacc + 2 + (T + 2) * PAIRS}"  # channel stride in bytes (in)
+    ROWB = f"%{nacc + 3 + (T + 2) * PAIRS}"  # row stride in bytes (in)
+    ncase = R * 9
+    tag = f"R{R}T{T}S{S}"
+    L = []
+    L.append("{")
+    L.append(".reg .b64 %%va, %%vb, %%ka, %%kb;")  # (v,v) and (case,0) of the current / next entry
+    L.append(".reg .b32 %%cn, %%sp, %%v1, %%vd, %%wa;")
+    L.append(".reg .f32 " + ", ".join(f"%%a{i}" for i in range(S)) + ", "
+             + ", ".join(f"%%x{i}" for i in range(S + 2)) + ";")
+    L.append(f"mov.b32 %%sp, {P};")
+    L.append("ld.shared.v2.b64 {%%va, %%ka}, [%%sp];")
+    L.append("ld.shared.v2.b64 {%%vb, %%kb}, [%%sp+16];")
+    L.append("add.u32 %%sp, %%sp, 32;")
+    L.append("cvt.u32.u64 %%cn, %%ka;")
+    L.append(f"$D{tag}_T: .branchtargets " + ", ".join(f"$D{tag}_{i}" for i in range(ncase + 2)) + ";")
+    L.append(f"brx.idx.uni %%cn, $D{tag}_T;")
+    for i in range(ncase):
+        r, ky, kx = i // 9, (i // 3) % 3, i % 3
+        L.append(f"$D{tag}_{i}:")
+        L.append("cvt.u32.u64 %%cn, %%kb;")  # case of entry k+1 (loaded one case ago)
+        if kx != 1:
+            for t in range(T):
+                for h in range(SH):
+                    L.append(f"fma.rn.f32x2 {A(r, t, h)}, %%va, {X(t + ky, h + kx // 2)}, {A(r, t, h)};")
+        else:
+            L.append("mov.b64 {%%v1, %%vd}, %%va;")
+            for t in range(T):
+                row = t + ky
+                for j in range(PAIRS):
+                    L.append(f"mov.b64 {{%%x{2 * j}, %%x{2 * j + 1}}}, {X(row, j)};")
+                for h in range(SH):
+                    L.append(f"mov.b64 {{%%a{2 * h}, %%a{2 * h + 1}}}, {A(r, t, h)};")
+                for s in range(S):
+                    L.append(f"fma.rn.f32 %%a{s}, %%v1, %%x{s + 1}, %%a{s};")
+                for h in range(SH):
+                    L.append(f"mov.b64 {A(r, t, h)}, {{%%a{2 * h}, %%a{2 * h + 1}}};")
+        L += tail()
+    # next channel: advance the window and reload it (T+2 rows of PAIRS pairs)
+    L.append(f"$D{tag}_{ncase}:")
+    L.append("cvt.u32.u64 %%cn, %%kb;")
+    L.append(f"add.u32 {WP}, {WP}, {CHS};")
+    L.append(f"mov.b32 %%wa, {WP};")
+    for i in range(T + 2):
+        j = 0
+        while j + 1 < PAIRS:
+            L.append(f"ld.shared.v2.b64 {{{X(i, j)}, {X(i, j + 1)}}}, [%%wa+{8 * j}];")
+            j += 2
+        if j < PAIRS:
+            L.append(f"ld.shared.b64 {X(i, j)}, [%%wa+{8 * j}];")
+        if i + 1 < T + 2:
+            L.append(f"add.u32 %%wa, %%wa, {ROWB};")
+    L += tail()
+    L.append(f"$D{tag}_{ncase + 1}:")
+    L.append(f"mov.b32 {P}, %%sp;")
+    L.append("}")
+    asm = "\\n\\t".join(L)
+    outs = ", ".join(f'"+l"(acc[{r}][{t}][{h}])' for r in range(R) for t in range(T) for h in range(SH))
+    xws = ", ".join(f'"+l"(xw[{i}][{j}])' for i in range(T + 2) for j in range(PAIRS))
+    return (f"#define SPC2_DISPATCH_{tag}(acc, xw, sp, wp, chs, rowb) \\\n"
+            f"    asm volatile(\"{asm}\" \\\n"
+            f"                 : {outs}, \"+r\"(sp), {xws}, \"+r\"(wp) \\\n"
+            f"                 : \"r\"(chs), \"r\"(rowb) \\\n"
+            f"                 : \"memory\")\n")
+
+
+def main(out_path: str) -> None:
+    text = ["// GENERATED by gen_dispatch2.py — do not edit.\n"]
+    for R, T, S in VARIANTS:
+        text.append(f"// R={R} rows, thread tile T={T} x S={S}, window {T + 2} x {S + 2} as 64-bit pairs.\n")
+        text.append(gen(R, T, S))
+    tmp = out_path + ".tmp"
+    with open(tmp, "w") as f:
+        f.write("\n".join(text))
+    os.replace(tmp, out_path)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else
+         os.path.join(os.path.dirname(os.path.abspath(__file__)), "dispatch2_gen.inc"))

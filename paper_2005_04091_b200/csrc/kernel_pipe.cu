@@ -1,0 +1,510 @@
+// kernel_pipe.cu — warp-specialised, TMA-pipelined CSR sparse direct
+// convolution for sm_100a (K = 3, stride 1, pad 1: the ResNet/VGG layers of
+// BASELINE.json), with the conv-only and the fused bias+ReLU+2x2-maxpool
+// epilogues.  This is the v2 ("pipe") kernel; kernel_tiled.cu is v1.
+//
+// What it computes is PAPER.md L393-401 (per output channel, per nonzero j of
+// its CSR row: out[n][y][x] += value[j] * in[...offset(colidx[j])]) under the
+// FP32 contract of include/spconv.h (ascending colidx, fma, bias after the
+// sum), so the result is bit-identical to the oracle.  How it maps to B200:
+//
+//  * CTA = GPC warps (<= 8, so 2 warps per SM sub-partition and up to 255
+//    registers each).  Warp w owns row
+//    group g = gset*GPC + w (R output channels with balanced nnz, SURVEY.md
+//    §8(a) a3; "register blocking"); lane l owns one 4x4
+//    output tile, so a thread accumulates R x 4 x 4 outputs in registers
+//    (64-bit pairs: packed FFMA2).  All warps of a CTA share the pixel block.
+//  * Staging (a4; "data prefetching"): one input channel per
+//    stage of an NSTAGE-deep shared-memory ring, filled with (i) the block's
+//    input rows + halo via one 4-D TMA tile load whose out-of-bounds zero
+//    fill is the padding (cp.async with zero fill when the TMA stride rule
+//    fails), and (ii) the CTA's decoded tap stream for that channel via one
+//    bulk copy, completing on the stage's "full" mbarrier.  There is no
+//    producer warp and no __syncthreads in the main loop: the LAST warp to
+//    finish with a stage (shared-memory counter) refills it, so no warp ever
+//    waits for a slower one except on data.
+//  * Consumer (a5): per channel, load the 6x6 window (LDS.128 + LDS.64 per
+//    row), then run the threaded-code dispatcher of dispatch2_gen.inc over
+//    the warp's entries {v, v, case}: one brx.idx per nonzero, the jump
+//    target of nonzero k+1 and the entry of k+2 fetched while k's FMAs issue.
+//  * Epilogue (a6): + bias and store; or ReLU, 2x2 max and first-max argmax
+//    (the conv output is never written).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "spconv_internal.h"
+
+namespace spconv {
+namespace {
+
+constexpr int MAXSTAGE = 8;
+constexpr int MAX_GPC = 8;
+
+struct PipeArgs {
+    const float *x;
+    float *y;
+    int32_t *argmax;
+    const float *bias;
+    const int32_t *group_rows;
+    const int32_t *chunk_start; // byte offsets of (gset, c) chunks in stream
+    const char *stream;
+    int N, C, H, W, F, Ho, Wo, Po, Qo;
+    int xs, tiles_x, tiles_y, ipb, tr, lanes, blocks_y, rs, pitch, nstage, in_words, in_pad, st_bytes;
+    int cc, nchunks;
+    int gpc, num_groups, num_gsets;
+    int tma;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0,
+                                            int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_4(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float(uint32_t(v)); }
+__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(uint32_t(v >> 32)); }
+
+#include "dispatch2_gen.inc"
+
+// Fill stage s with input channel k (and the CTA's stream chunk of k).  TMA:
+// called by one lane.  cp.async: called by a whole warp.
+template <int XS>
+__device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeArgs &a, uint32_t smem0,
+                                           uint32_t fb, int s, int k, int n0, int iy0, const int32_t *cstart,
+                                           int lane) {
+    const uint32_t stage_bytes = uint32_t(a.in_pad + a.st_bytes);
+    const uint32_t dst_in = smem0 + uint32_t(s) * stage_bytes;
+    const uint32_t dst_st = dst_in + uint32_t(a.in_pad);
+    // k = stage index: channels [k*cc, k*cc + cc)
+    const int c_beg = __ldg(cstart + k), c_end = __ldg(cstart + k + 1);
+    const uint32_t st_bytes = uint32_t(c_end - c_beg);
+    // order the consumers' generic-proxy reads of this stage before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if constexpr (XS == 3) {
+        mbar_expect_tx(fb, uint32_t(a.in_words) * 4u + st_bytes);
+        tma_load_4d(tmap, fb, dst_in, -(XS + 1), iy0, k * a.cc, n0);
+        bulk_load(dst_st, a.stream + c_beg, st_bytes, fb);
+    } else {
+        if (lane == 0) {
+            mbar_expect_tx(fb, st_bytes);
+            bulk_load(dst_st, a.stream + c_beg, st_bytes, fb);
+        }
+        // smem layout of a stage = the TMA box order [image][channel][row][col]
+        const int per_ch = a.rs * a.pitch, per_img = a.cc * per_ch;
+        for (int e = lane; e < a.in_words; e += 32) {
+            const int im = e / per_img;
+            int rem = e - im * per_img;
+            const int cl = rem / per_ch;
+            rem -= cl * per_ch;
+            const int r = rem / a.pitch, col = rem - r * a.pitch;
+            const int n = n0 + im, c = k * a.cc + cl, iy = iy0 + r, ix = col - (XS + 1);
+            const bool ok = n < a.N && c < a.C && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+            const float *src = ok ? a.x + (((size_t)n * a.C + c) * a.H + iy) * a.W + ix : a.x;
+            cp_async_4(dst_in + uint32_t(e) * 4u, src, ok);
+        }
+        cp_async_arrive_noinc(fb);
+    }
+}
+
+template <int R, int PT, int PS, bool FUSED, int XS>
+__global__ void __launch_bounds__(32 * MAX_GPC, 1)
+    pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full_bar[MAXSTAGE];
+    __shared__ int done_cnt[MAXSTAGE];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int bid = blockIdx.x;
+    const int gs = bid % a.num_gsets;
+    bid /= a.num_gsets;
+    const int by = bid % a.blocks_y;
+    const int n0 = (bid / a.blocks_y) * a.ipb; // first image of the block
+    const int ty0 = by * a.tr;                 // first tile row of the block
+    const int nconsumers = min(a.gpc, a.num_groups - gs * a.gpc);
+    const int ns = a.nstage;
+    const uint32_t stage_bytes = uint32_t(a.in_pad + a.st_bytes);
+    const uint32_t smem0 = smem_u32(smem);
+    const int iy0 = ty0 * PT - 1; // first staged input row (pad = 1)
+    const int32_t *cstart = a.chunk_start + (size_t)gs * (a.nchunks + 1);
+    if (warp >= nconsumers) return; // whole warp exits before any barrier use
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(smem_u32(&full_bar[s]), XS == 3 ? 1u : 33u);
+            done_cnt[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (warp == 0) {
+        // prologue: fill the first stages
+        for (int k = 0; k < min(ns, a.nchunks); ++k) {
+            if (XS == 3 && lane != 0) continue;
+            fill_stage<XS>(&tmap, a, smem0, smem_u32(&full_bar[k]), k, k, n0, iy0, cstart, lane);
+        }
+    }
+    // all consumer warps must see the initialised barriers (bar.sync over nconsumers warps)
+    asm volatile("bar.sync 1, %0;" ::"r"(nconsumers * 32) : "memory");
+
+    // ---------------- consumer warps ----------------
+    const int g = gs * a.gpc + warp;
+    const int per_img_tiles = a.tr * a.tiles_x;
+    const bool lane_ok = lane < a.lanes;
+    const int li = lane_ok ? lane : 0;
+    const int im = li / per_img_tiles;
+    const int rem = li - im * per_img_tiles;
+    const int tyl = rem / a.tiles_x, tx = rem - tyl * a.tiles_x;
+    // word offset of this thread's 6x6 window inside a stage (16-byte aligned)
+    const uint32_t win_off = uint32_t((im * a.cc * a.rs + tyl * PT) * a.pitch + tx * PS) * 4u;
+    const uint32_t row_bytes = uint32_t(a.pitch) * 4u;
+    const uint32_t ch_bytes = uint32_t(a.rs * a.pitch) * 4u;
+
+    constexpr int SH = PS / 2, PAIRS = (PS + 2) / 2;
+    uint64_t acc[R][PT][SH];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int t = 0; t < PT; ++t)
+#pragma unroll
+            for (int h = 0; h < SH; ++h) acc[r][t][h] = 0ull;
+
+    for (int k = 0; k < a.nchunks; ++k) {
+        const int s = k % ns;
+        mbar_wait(smem_u32(&full_bar[s]), (k / ns) & 1);
+        const unsigned char *stage = smem + size_t(s) * stage_bytes;
+        const uint32_t st_base = smem0 + uint32_t(s) * stage_bytes + uint32_t(a.in_pad);
+        uint32_t sp = st_base + reinterpret_cast<const uint32_t *>(stage + a.in_pad)[warp];
+        uint32_t wp = smem0 + uint32_t(s) * stage_bytes + win_off; // window of the stage's first channel
+        uint64_t xw[PT + 2][PAIRS];
+        const unsigned char *wptr = stage + win_off;
+#pragma unroll
+        for (int i = 0; i < PT + 2; ++i) {
+#pragma unroll
+            for (int j = 0; j + 1 < PAIRS; j += 2) {
+                const ulonglong2 q = *reinterpret_cast<const ulonglong2 *>(wptr + i * row_bytes + 16 * (j / 2));
+                xw[i][j] = q.x;
+                xw[i][j + 1] = q.y;
+            }
+            if constexpr (PAIRS % 2)
+                xw[i][PAIRS - 1] = *reinterpret_cast<const uint64_t *>(wptr + i * row_bytes + 8 * (PAIRS - 1));
+        }
+        // one walk over the stage's channels: taps, "next channel" (window reload), end
+        static_assert(R == 4 && PT == 4 && PS == 8, "no dispatcher generated for this variant");
+        SPC2_DISPATCH_R4T4S8(acc, xw, sp, wp, ch_bytes, row_bytes);
+
+        // release stage s: the last warp to finish with it refills it with channel k + ns
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            // monotonic: the n-th use of stage s completes when the count reaches n*nconsumers
+            const int old = atomicAdd(&done_cnt[s], 1);
+            last = (old % nconsumers) == nconsumers - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last && k + ns < a.nchunks) {
+            if (XS == 0 || lane == 0)
+                fill_stage<XS>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, k + ns, n0, iy0, cstart, lane);
+        }
+    }
+
+    // ---------------- epilogue (a6) ----------------
+    const int n = n0 + im;
+    const int ty = ty0 + tyl;
+    const bool out_ok = lane_ok && n < a.N && ty < a.tiles_y;
+    const int oy0 = ty * PT, ox0 = tx * PS - XS;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int f = __ldg(a.group_rows + g * R + r);
+        if (f < 0) continue; // warp-uniform
+        const float b = __ldg(a.bias + f);
+        float v[PT][PS];
+#pragma unroll
+        for (int t = 0; t < PT; ++t)
+#pragma unroll
+            for (int h = 0; h < SH; ++h) {
+                v[t][2 * h] = __fadd_rn(lo_f(acc[r][t][h]), b);
+                v[t][2 * h + 1] = __fadd_rn(hi_f(acc[r][t][h]), b);
+            }
+        if constexpr (!FUSED) {
+            if (!out_ok) continue;
+            float *yp = a.y + ((size_t)n * a.F + f) * a.Ho * a.Wo;
+#pragma unroll
+            for (int t = 0; t < PT; ++t) {
+                const int oy = oy0 + t;
+                if (oy >= a.Ho) continue;
+                float *row = yp + (size_t)oy * a.Wo;
+                if (XS == 0 && ox0 + PS <= a.Wo && ((reinterpret_cast<uintptr_t>(row + ox0) & 15) == 0) &&
+                    (a.Wo & 3) == 0) {
+#pragma unroll
+                    for (int q = 0; q < PS; q += 4)
+                        *reinterpret_cast<float4 *>(row + ox0 + q) =
+                            make_float4(v[t][q], v[t][q + 1], v[t][q + 2], v[t][q + 3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PS; ++q) {
+                        const int ox = ox0 + q;
+                        if (ox >= 0 && ox < a.Wo) row[ox] = v[t][q];
+                    }
+                }
+            }
+        } else {
+            // ReLU then 2x2 max with first-max argmax (row-major window order).
+            // XS == 0: the pairs (0,1), (2,3), ... of the tile are lane-local.  XS == 3:
+            // the tile covers columns PS*tx-3 .. PS*tx+PS-4; pairs (1,2), (3,4), ... are
+            // local and the last pair (PS-1, PS) takes column PS*tx+PS-3 from the next
+            // lane (the pair (-1, 0) is the previous lane's).  A lane whose neighbour
+            // is another tile row never needs it: its last pair starts at >= Wo - 1.
+            float rl[PT][PS + 1];
+#pragma unroll
+            for (int t = 0; t < PT; ++t) {
+#pragma unroll
+                for (int q = 0; q < PS; ++q) rl[t][q] = v[t][q] > 0.0f ? v[t][q] : 0.0f;
+                rl[t][PS] = XS ? __shfl_down_sync(0xffffffffu, rl[t][0], 1) : 0.0f;
+            }
+            if (!out_ok) continue;
+            float *yp = a.y + ((size_t)n * a.F + f) * a.Po * a.Qo;
+            int32_t *ap = a.argmax ? a.argmax + ((size_t)n * a.F + f) * a.Po * a.Qo : nullptr;
+#pragma unroll
+            for (int tp = 0; tp < PT / 2; ++tp) {
+                const int py = (oy0 >> 1) + tp;
+                if (py >= a.Po) continue;
+#pragma unroll
+                for (int pp = 0; pp < PS / 2; ++pp) {
+                    const int q0 = XS ? 2 * pp + 1 : 2 * pp;
+                    const int ox = ox0 + q0;
+                    if (ox < 0) continue;
+                    const int px = ox >> 1;
+                    if (px >= a.Qo) continue;
+                    float best = 0.0f;
+                    int bidx = 0;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int dy = w >> 1, dx = w & 1;
+                        const float rv = rl[2 * tp + dy][q0 + dx];
+                        if (w == 0 || rv > best) {
+                            best = rv;
+                            bidx = (oy0 + 2 * tp + dy) * a.Wo + ox + dx;
+                        }
+                    }
+                    yp[(size_t)py * a.Qo + px] = best;
+                    if (ap) ap[(size_t)py * a.Qo + px] = bidx;
+                }
+            }
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int R, int PT, int PS, bool FUSED, int XS>
+cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size_t smem, cudaStream_t s) {
+    auto kern = pipe_kernel<R, PT, PS, FUSED, XS>;
+    static size_t attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    size_t &done = attr_done[dev & 63];
+    if (smem > 48 * 1024 && __atomic_load_n(&done, __ATOMIC_ACQUIRE) < smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        __atomic_store_n(&done, smem, __ATOMIC_RELEASE);
+    }
+    kern<<<grid, 32 * a.gpc, smem, s>>>(map, a);
+    return cudaGetLastError();
+}
+
+// Shared-memory wavefronts of one warp-wide window row load (LDS.128 at the
+// window start + LDS.64 at +16 B) for a candidate pitch: quarter-warp phases
+// for 16-byte accesses, half-warp phases for 8-byte accesses; the degree of a
+// phase is the largest number of distinct addresses that share a bank.
+int window_wavefronts(const PipeGeometry &g, int pitch) {
+    const int PT = g.T, PS = g.S;
+    int addr[32];
+    const int per_img = g.tr * g.tiles_x;
+    for (int l = 0; l < 32; ++l) {
+        const int li = l < g.lanes ? l : 0;
+        const int im = li / per_img, rem = li % per_img;
+        const int tyl = rem / g.tiles_x, tx = rem % g.tiles_x;
+        addr[l] = (im * g.rs + tyl * PT) * pitch + tx * PS; // words
+    }
+    int total = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int width = pass == 0 ? 4 : 2, group = pass == 0 ? 8 : 16, off = pass == 0 ? 0 : PS;
+        for (int p0 = 0; p0 < 32; p0 += group) {
+            int worst = 1;
+            for (int bank = 0; bank < 32; ++bank) {
+                int distinct[32], nd = 0;
+                for (int l = p0; l < p0 + group; ++l) {
+                    for (int w = 0; w < width; ++w) {
+                        const int word = addr[l] + off + w;
+                        if ((word & 31) != bank) continue;
+                        bool seen = false;
+                        for (int d = 0; d < nd; ++d) seen |= distinct[d] == word;
+                        if (!seen) distinct[nd++] = word;
+                    }
+                }
+                worst = std::max(worst, nd);
+            }
+            total += worst;
+        }
+    }
+    return total;
+}
+
+} // namespace
+
+bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {
+    (void)C; (void)F; (void)H;
+    // 4x8 tiles, whole tile rows per block: at most 32 tiles across.  AUTO uses this
+    // kernel only where TMA can stage the input (16-byte row stride); the cp.async
+    // fallback inside it remains for misaligned input pointers.
+    return K == 3 && stride == 1 && pad == 1 && W + 3 <= 8 * 32 && (W * 4) % 16 == 0;
+}
+
+void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g) {
+    g = PipeGeometry{};
+    g.xs = tma ? 3 : 0;
+    g.T = 4;
+    g.S = 8; // 4x8 tiles: 16 FFMA2 per nonzero (scripts/probes/dispatch_probe.cu)
+    const int PT = g.T, PS = g.S;
+    g.tiles_x = (p.Wo + g.xs + PS - 1) / PS;
+    g.tiles_y = (p.Ho + PT - 1) / PT;
+    if (g.tiles_x > 32) return;
+    const int per_img = g.tiles_x * g.tiles_y;
+    if (per_img <= 16) {
+        g.ipb = 32 / per_img;
+        g.tr = g.tiles_y;
+    } else {
+        g.ipb = 1;
+        g.tr = std::min(g.tiles_y, 32 / g.tiles_x);
+    }
+    g.lanes = g.ipb * g.tr * g.tiles_x;
+    g.blocks_y = (g.tiles_y + g.tr - 1) / g.tr;
+    g.rs = PT * g.tr + 2;
+    // smem columns read: window of the last tile ends at 4*(tiles_x-1) + 5
+    const int need = ((PS * g.tiles_x + 2) + 3) & ~3;
+    int best = need, best_wf = 1 << 30;
+    for (int cand = need; cand <= need + 32; cand += 4) {
+        const int wf = window_wavefronts(g, cand);
+        if (wf < best_wf) {
+            best_wf = wf;
+            best = cand;
+        }
+    }
+    g.pitch = best;
+    if (tma && (g.pitch > 256 || g.rs > 256 || (p.W * 4) % 16 != 0)) return;
+    g.cc = p.pipe_cc;
+    g.nchunks = (p.C + g.cc - 1) / g.cc;
+    g.in_words = g.ipb * g.cc * g.rs * g.pitch;
+    g.in_pad = (g.in_words * 4 + 127) & ~127;
+    g.st_bytes = (p.max_chunk_bytes + 32 + 127) & ~127; // + 2 entries of look-ahead slack
+    const int stage_bytes = g.in_pad + g.st_bytes;
+    const int budget = 200 * 1024;
+    g.nstage = std::min(MAXSTAGE, budget / stage_bytes);
+    if (g.nstage < 2) return;
+    g.smem_bytes = size_t(g.nstage) * stage_bytes;
+    g.ok = true;
+}
+
+cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
+                        cudaStream_t s) {
+    bool use_tma = p.pipe_tma.ok && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && get_encode() != nullptr;
+    const PipeGeometry &g = use_tma ? p.pipe_tma : p.pipe_cp;
+    if (!g.ok) return cudaErrorInvalidConfiguration;
+    PipeArgs a;
+    a.x = x; a.y = y; a.argmax = argmax;
+    a.bias = p.d_bias; a.group_rows = p.d_group_rows; a.chunk_start = p.d_chunk_start;
+    a.stream = reinterpret_cast<const char *>(p.d_stream2);
+    a.N = N; a.C = p.C; a.H = p.H; a.W = p.W; a.F = p.F; a.Ho = p.Ho; a.Wo = p.Wo;
+    a.Po = p.Ho / 2; a.Qo = p.Wo / 2;
+    a.xs = g.xs; a.tiles_x = g.tiles_x; a.tiles_y = g.tiles_y; a.ipb = g.ipb; a.tr = g.tr;
+    a.lanes = g.lanes; a.blocks_y = g.blocks_y; a.rs = g.rs; a.pitch = g.pitch; a.nstage = g.nstage;
+    a.in_words = g.in_words; a.in_pad = g.in_pad; a.st_bytes = g.st_bytes;
+    a.cc = g.cc; a.nchunks = g.nchunks;
+    a.gpc = p.gpc; a.num_groups = p.num_groups; a.num_gsets = p.num_gsets;
+    a.tma = use_tma ? 1 : 0;
+    const int64_t grid64 = (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y * p.num_gsets;
+    if (grid64 > 0x7fffffff) return cudaErrorInvalidConfiguration;
+
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if (use_tma) {
+        cuuint64_t dims[4] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)N};
+        cuuint64_t strides[3] = {(cuuint64_t)p.W * 4, (cuuint64_t)p.H * p.W * 4,
+                                 (cuuint64_t)p.C * p.H * p.W * 4};
+        cuuint32_t box[4] = {(cuuint32_t)g.pitch, (cuuint32_t)g.rs, (cuuint32_t)g.cc, (cuuint32_t)g.ipb};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), dims,
+                                  strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+    const int grid = int(grid64);
+#define SPC_PIPE_LAUNCH(RR, TT, SS)                                                                 \
+    if (p.R == RR && g.T == TT && g.S == SS) {                                                      \
+        if (use_tma) return fused ? launch_one<RR, TT, SS, true, 3>(map, a, grid, g.smem_bytes, s)  \
+                                  : launch_one<RR, TT, SS, false, 3>(map, a, grid, g.smem_bytes, s); \
+        return fused ? launch_one<RR, TT, SS, true, 0>(map, a, grid, g.smem_bytes, s)               \
+                     : launch_one<RR, TT, SS, false, 0>(map, a, grid, g.smem_bytes, s);             \
+    }
+    SPC_PIPE_LAUNCH(4, 4, 8)
+#undef SPC_PIPE_LAUNCH
+    return cudaErrorInvalidValue;
+}
+
+} // namespace spconv

@@ -80,6 +80,8 @@ void free_plan(Plan *p) {
     cudaFree(p->d_group_rows);
     cudaFree(p->d_segoff);
     cudaFree(p->d_stream);
+    cudaFree(p->d_chunk_start);
+    cudaFree(p->d_stream2);
     cudaFree(p->d_xbuf);
     cudaFree(p->d_ybuf);
     cudaFree(p->d_abuf);
@@ -148,12 +150,91 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
     if ((st = upload(&p->d_values, values.data(), values.size(), p->device_bytes))) return st;
     if ((st = upload(&p->d_bias, bias.data(), bias.size(), p->device_bytes))) return st;
 
-    if (p->kernel != SPCONV_KERNEL_TILED) return SPCONV_OK;
-    // a3: balanced row groups and the per-(group, channel) tap streams
+    if (p->kernel == SPCONV_KERNEL_GENERIC) return SPCONV_OK;
+    // a3: balanced row groups
     const int R = rows_per_group;
     p->R = R;
     std::vector<int32_t> grows = balance_groups(rowptr, p->F, R, p->num_groups);
     const int C = p->C;
+    if (p->kernel == SPCONV_KERNEL_PIPE) {
+        // Per (group set, pipeline stage of cc channels) chunk: a header of GPC u32
+        // byte offsets (one per warp, 16-byte padded) then, per warp, for each channel
+        // of the stage its group's nonzeros as 16-byte entries {v, v, case = r*9 +
+        // ky*3 + kx, 0} ascending by case, followed by a "next channel" marker (case
+        // R*9) or, after the stage's last channel, an "end" marker (R*9+1).
+        // Ascending case within a channel, channels in order: every output row's
+        // taps are consumed in ascending colidx order (the FP32 contract).
+        p->gpc = std::min(p->num_groups, 8);
+        p->num_gsets = (p->num_groups + p->gpc - 1) / p->gpc;
+        const int hdr = ((p->gpc * 4 + 15) / 16) * 16;
+        std::vector<uint4> out;
+        // per group: per channel list of (case, value)
+        std::vector<std::vector<std::vector<std::pair<int, float>>>> byc(size_t(p->num_groups));
+        for (int g = 0; g < p->num_groups; ++g) {
+            byc[size_t(g)].resize(size_t(C));
+            for (int r = 0; r < R; ++r) {
+                const int f = grows[size_t(g) * R + r];
+                if (f < 0) continue;
+                for (int32_t j = rowptr[f]; j < rowptr[f + 1]; ++j) {
+                    const int col = colidx[size_t(j)];
+                    const int c = col / 9, ky = (col / 3) % 3, kx = col % 3;
+                    byc[size_t(g)][size_t(c)].push_back({r * 9 + ky * 3 + kx, values[size_t(j)]});
+                }
+            }
+        }
+        // channels per stage: about 20 KB of staged input per stage
+        p->pipe_cc = 1;
+        p->max_chunk_bytes = 0;
+        spconv::pipe_geometry(*p, false, p->pipe_cp);
+        spconv::pipe_geometry(*p, true, p->pipe_tma);
+        const int per_ch = std::max(p->pipe_tma.in_words, p->pipe_cp.in_words) * 4;
+        p->pipe_cc = std::max(1, std::min({8, C, 20480 / std::max(per_ch, 1)}));
+        const int cc = p->pipe_cc, nchunks = (C + cc - 1) / cc;
+        const uint32_t NEXT = uint32_t(R * 9), END = uint32_t(R * 9 + 1);
+        std::vector<int32_t> cstart(size_t(p->num_gsets) * (nchunks + 1));
+        int maxb = 0;
+        for (int gs = 0; gs < p->num_gsets; ++gs) {
+            for (int j = 0; j < nchunks; ++j) {
+                const size_t base = out.size();
+                cstart[size_t(gs) * (nchunks + 1) + j] = int32_t(base * 16);
+                out.resize(base + size_t(hdr / 16));
+                std::vector<uint32_t> offs(size_t(p->gpc), 0);
+                const int c0 = j * cc, c1 = std::min(C, c0 + cc);
+                for (int w = 0; w < p->gpc; ++w) {
+                    const int g = gs * p->gpc + w;
+                    offs[size_t(w)] = uint32_t((out.size() - base) * 16);
+                    for (int c = c0; c < c1; ++c) {
+                        if (g < p->num_groups) {
+                            auto v = byc[size_t(g)][size_t(c)];
+                            std::stable_sort(v.begin(), v.end(),
+                                             [](const std::pair<int, float> &a, const std::pair<int, float> &b) {
+                                                 return a.first < b.first;
+                                             });
+                            for (auto &e : v) {
+                                uint32_t bits;
+                                std::memcpy(&bits, &e.second, 4);
+                                out.push_back(make_uint4(bits, bits, uint32_t(e.first), 0u));
+                            }
+                        }
+                        out.push_back(make_uint4(0u, 0u, c + 1 < c1 ? NEXT : END, 0u));
+                    }
+                }
+                std::memcpy(reinterpret_cast<char *>(out.data() + base), offs.data(), offs.size() * 4);
+                maxb = std::max(maxb, int((out.size() - base) * 16));
+            }
+            cstart[size_t(gs) * (nchunks + 1) + nchunks] = int32_t(out.size() * 16);
+        }
+        if (out.size() * 16 > size_t(INT32_MAX)) return SPCONV_ERR_UNSUPPORTED;
+        p->max_chunk_bytes = maxb;
+        if ((st = upload(&p->d_group_rows, grows.data(), grows.size(), p->device_bytes))) return st;
+        if ((st = upload(&p->d_chunk_start, cstart.data(), cstart.size(), p->device_bytes))) return st;
+        if ((st = upload(&p->d_stream2, out.data(), out.size(), p->device_bytes))) return st;
+        spconv::pipe_geometry(*p, true, p->pipe_tma);
+        spconv::pipe_geometry(*p, false, p->pipe_cp);
+        if (!p->pipe_cp.ok) return SPCONV_ERR_UNSUPPORTED;
+        return SPCONV_OK;
+    }
+    // tiled (v1): per (group, channel) tap streams
     std::vector<int32_t> segoff(size_t(p->num_groups) * (C + 1));
     std::vector<spconv::TapEntry> stream;
     stream.reserve(size_t(p->nnz) + size_t(p->num_groups) * C);
@@ -226,7 +307,7 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
     if (Hp < K || Wp < K) return SPCONV_ERR_SHAPE;
     spconv_options_t o{};
     if (opts) o = *opts;
-    if (o.kernel < SPCONV_KERNEL_AUTO || o.kernel > SPCONV_KERNEL_TILED) return SPCONV_ERR_UNSUPPORTED;
+    if (o.kernel < SPCONV_KERNEL_AUTO || o.kernel > SPCONV_KERNEL_PIPE) return SPCONV_ERR_UNSUPPORTED;
     for (int r : o.reserved)
         if (r != 0) return SPCONV_ERR_UNSUPPORTED;
 
@@ -274,15 +355,20 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
     p->nnz = nnz;
     p->device = device;
     const bool tiled_ok = spconv::tiled_supported(C, H, W, F, K, stride, pad);
-    if (o.kernel == SPCONV_KERNEL_TILED && !tiled_ok) {
+    const bool pipe_ok = spconv::pipe_supported(C, H, W, F, K, stride, pad);
+    if ((o.kernel == SPCONV_KERNEL_TILED && !tiled_ok) || (o.kernel == SPCONV_KERNEL_PIPE && !pipe_ok)) {
         delete p;
         return SPCONV_ERR_UNSUPPORTED;
     }
-    p->kernel = (o.kernel == SPCONV_KERNEL_GENERIC || !tiled_ok) ? SPCONV_KERNEL_GENERIC
-                                                                : SPCONV_KERNEL_TILED;
+    if (o.kernel == SPCONV_KERNEL_AUTO)
+        p->kernel = pipe_ok ? SPCONV_KERNEL_PIPE : tiled_ok ? SPCONV_KERNEL_TILED : SPCONV_KERNEL_GENERIC;
+    else
+        p->kernel = o.kernel;
     int R = o.rows_per_group;
-    if (R == 0) R = spconv::tiled_default_R(C, F, double(nnz) / (double(F) * ncol));
-    if (p->kernel == SPCONV_KERNEL_TILED && R != 4 && R != 8) {
+    if (R == 0)
+        R = p->kernel == SPCONV_KERNEL_PIPE ? 4 : spconv::tiled_default_R(C, F, double(nnz) / (double(F) * ncol));
+    if ((p->kernel == SPCONV_KERNEL_PIPE && R != 4) ||
+        (p->kernel == SPCONV_KERNEL_TILED && R != 4 && R != 8)) {
         delete p;
         return SPCONV_ERR_UNSUPPORTED;
     }
@@ -326,7 +412,9 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     if (!guard.ok) return SPCONV_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e;
-    if (p->kernel == SPCONV_KERNEL_TILED)
+    if (p->kernel == SPCONV_KERNEL_PIPE)
+        e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s);
+    else if (p->kernel == SPCONV_KERNEL_TILED)
         e = spconv::launch_tiled(*p, N, x, y, argmax, fused, s);
     else
         e = fused ? spconv::launch_generic_fused(*p, N, x, y, argmax, s)

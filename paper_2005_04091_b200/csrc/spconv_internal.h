@@ -39,6 +39,28 @@ struct TiledGeometry {
     size_t smem_bytes;
 };
 
+// Geometry of the warp-specialised pipeline kernel (kernel_pipe.cu) for one
+// staging path: TMA (xs = 3: tile columns start at 4*tx - 3 so that the
+// 16-byte-aligned TMA box start ix = -4 puts each window on a 16-byte smem
+// boundary) or cp.async (xs = 0: the box starts at ix = -1).
+struct PipeGeometry {
+    bool ok = false;
+    int xs;                  // column shift of the thread tiles (3: TMA, 0: cp.async)
+    int T, S;                // thread tile: T output rows x S output columns
+    int tiles_x, tiles_y;    // 4x4 thread tiles per image row / column
+    int ipb, tr;             // images per block, tile rows per block (per image)
+    int lanes;               // active lanes per consumer warp = ipb * tr * tiles_x
+    int blocks_y;            // blocks per image (ipb == 1) along the tile rows
+    int rs;                  // staged input rows per image = 4 * tr + 2
+    int pitch;               // smem words per staged row (multiple of 4)
+    int nstage;              // pipeline depth
+    int cc, nchunks;         // input channels per stage, stages per pass
+    int in_words;            // words of one stage's input box = ipb * rs * pitch
+    int in_pad;              // bytes reserved for it (128-byte multiple)
+    int st_bytes;            // bytes reserved per stage for the stream chunk
+    size_t smem_bytes;       // dynamic shared memory per CTA
+};
+
 struct Plan {
     int C, H, W, F, K, stride, pad, Ho, Wo;
     int64_t nnz;
@@ -57,6 +79,13 @@ struct Plan {
     int32_t *d_segoff = nullptr;     // [num_groups * (C + 1)] offsets into d_stream
     TapEntry *d_stream = nullptr;    // [nnz + num_groups*C]: per (group, channel) taps + sentinel
     TiledGeometry geo{};
+    // pipeline (v2) path: GPC consumer warps per CTA, one row group each
+    int gpc = 0, num_gsets = 0;
+    int max_chunk_bytes = 0;       // largest (gset, stage) stream chunk incl. header
+    int pipe_cc = 1;               // input channels per pipeline stage
+    int32_t *d_chunk_start = nullptr; // [num_gsets * (nchunks + 1)] byte offsets into d_stream2
+    uint4 *d_stream2 = nullptr;    // chunks: header (GPC u32 byte offsets) + 16-byte entries
+    PipeGeometry pipe_tma{}, pipe_cp{};
     int64_t device_bytes = 0;
     // spconv_forward_host staging
     std::mutex host_mu;
@@ -70,6 +99,12 @@ struct Plan {
 cudaError_t launch_generic_conv(const Plan &p, int N, const float *x, float *y, cudaStream_t s);
 cudaError_t launch_generic_fused(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                                  cudaStream_t s);
+
+// kernel_pipe.cu
+bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad);
+void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g);
+cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
+                        bool fused, cudaStream_t s);
 
 // kernel_tiled.cu
 bool tiled_supported(int C, int H, int W, int F, int K, int stride, int pad);

@@ -18,8 +18,8 @@ LIB_PATH = os.path.join(_PKG, "libspconv.so")
 SPCONV_OK = 0
 STATUS = {0: "OK", -1: "NULLPTR", -2: "SHAPE", -3: "CSR", -4: "UNSUPPORTED", -5: "ALIGN",
           -6: "DEVICE", -7: "CUDA", -8: "OOM", -9: "ALIAS"}
-KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TILED = 0, 1, 2
-KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED}
+KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TILED, KERNEL_PIPE = 0, 1, 2, 3
+KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED, "pipe": KERNEL_PIPE}
 
 # Every symbol include/spconv.h declares (checked by tests/test_abi.py).
 EXPORTS = ("spconv_create", "spconv_create_ex", "spconv_forward", "spconv_fused_relu_maxpool",

@@ -17,7 +17,7 @@ from tests._util import allclose_contract, bits
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-KERNELS = ["tiled", "generic"]
+KERNELS = ["pipe", "tiled", "generic"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -30,8 +30,15 @@ def _gpu():
 
 def _layer(cfg, csr, bias, kernel):
     from paper_2005_04091_b200 import SparseConv2d
-    return SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, cfg.K, cfg.stride, cfg.pad, csr.rowptr,
-                        csr.colidx, csr.values, bias, device=0, kernel=kernel)
+    from paper_2005_04091_b200.spconv import SpconvError
+    try:
+        return SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, cfg.K, cfg.stride, cfg.pad, csr.rowptr,
+                            csr.colidx, csr.values, bias, device=0, kernel=kernel)
+    except SpconvError as e:
+        # the pipelined kernel needs a 16-byte input row stride (TMA); AUTO falls back
+        if kernel == "pipe" and e.status == -4 and (cfg.W * 4) % 16 != 0:
+            pytest.skip("pipe kernel: input row stride is not a multiple of 16 bytes")
+        raise
 
 
 def _bias(cfg):
