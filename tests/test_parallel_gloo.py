@@ -1,0 +1,152 @@
+"""Multi-process host logic of the batch-sharded driver,
+world_size 2 over gloo on CPU: sharding, CSR broadcast, output all-gather.
+
+The per-rank layer is injected (``layer_factory``); here it is the CPU oracle, so the
+test checks the distribution logic (every image computed exactly once, gathered in
+order, filters identical on every rank) — the CUDA forward itself is covered by the
+-m gpu parity tests and by bench.py under torchrun on the box.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+import oracle  # noqa: E402
+import synthgen  # noqa: E402
+from paper_2005_04091_b200.parallel import (ShardedSparseConv2d, broadcast_csr,  # noqa: E402
+                                            gather_output, shard_bounds)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class _OracleLayer:
+    """CPU stand-in for SparseConv2d (test-only)."""
+
+    def __init__(self, cfg, rp, ci, vv, b):
+        self.cfg = cfg
+        self.args = (cfg.F, cfg.K, cfg.stride, cfg.pad, rp.numpy(), ci.numpy(), vv.numpy(),
+                     None if b is None else b.numpy())
+
+    def __call__(self, x):
+        return torch.from_numpy(oracle.conv_f32(x.numpy(), *self.args))
+
+    def fused_relu_maxpool(self, x):
+        p, a = oracle.fused_f32(x.numpy(), *self.args)
+        return torch.from_numpy(p), torch.from_numpy(a)
+
+
+def _worker(rank, world, port, n_total, fused, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synthgen.CONFIGS["c1"].with_batch(n_total)
+        L = synthgen.make_layer(cfg)
+        bias = synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3))
+        src = (L.csr.rowptr, L.csr.colidx, L.csr.values, bias) if rank == 0 else (None, None, None, None)
+        layer = ShardedSparseConv2d(cfg.F, *src, device=torch.device("cpu"),
+                                    layer_factory=lambda rp, ci, vv, b: _OracleLayer(cfg, rp, ci, vv, b))
+        b0, b1 = layer.local_shard(n_total)
+        x_shard = torch.from_numpy(L.x[b0:b1].copy())
+        out = layer.forward_gather(x_shard, n_total, fused=fused)
+        if rank == 0:
+            if fused:
+                q.put((out[0].numpy(), out[1].numpy()))
+            else:
+                q.put(out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_total,fused", [(4, False), (5, False), (3, True)])
+def test_sharded_forward_gather_equals_single_process(n_total, fused):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_total, fused, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = synthgen.CONFIGS["c1"].with_batch(n_total)
+    L = synthgen.make_layer(cfg)
+    bias = synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3))
+    args = (L.x, cfg.F, cfg.K, cfg.stride, cfg.pad, L.csr.rowptr, L.csr.colidx, L.csr.values, bias)
+    if fused:
+        rp, ra = oracle.fused_f32(*args)
+        assert np.array_equal(got[0].view(np.uint32), rp.view(np.uint32))
+        assert np.array_equal(got[1], ra)
+    else:
+        ref = oracle.conv_f32(*args)
+        assert got.shape == ref.shape
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def _bcast_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synthgen.CONFIGS["c2"]
+        L = synthgen.make_layer(cfg, with_input=False)
+        if rank == 0:
+            rp, ci, vv, b = broadcast_csr(L.csr.rowptr, L.csr.colidx, L.csr.values, None, cfg.F, "cpu")
+        else:
+            rp, ci, vv, b = broadcast_csr(None, None, None, None, cfg.F, "cpu")
+        q.put((rank, rp.numpy(), ci.numpy(), vv.numpy(), b))
+        # uneven gather: 3 images over 2 ranks
+        y = torch.full((shard_bounds(3, world, rank)[1] - shard_bounds(3, world, rank)[0], 2), float(rank))
+        g = gather_output(y, 3)
+        q.put((rank, g.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_csr_and_uneven_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    items = [q.get(timeout=120) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    L = synthgen.make_layer(synthgen.CONFIGS["c2"], with_input=False)
+    csr_items = [it for it in items if len(it) == 5]
+    gath = [it for it in items if len(it) == 2]
+    assert len(csr_items) == 2 and len(gath) == 2
+    for _, rp, ci, vv, b in csr_items:
+        assert np.array_equal(rp, L.csr.rowptr)
+        assert np.array_equal(ci, L.csr.colidx)
+        assert np.array_equal(vv.view(np.uint32), L.csr.values.view(np.uint32))
+        assert b is None
+    for _, g in gath:
+        # rank 0 owns images [0, 2), rank 1 owns [2, 3)
+        assert np.array_equal(g[:, 0], np.array([0.0, 0.0, 1.0], np.float32))
+
+
+@pytest.mark.parametrize("n,world", [(0, 1), (7, 1), (7, 2), (8, 4), (3, 8), (256, 8)])
+def test_shard_bounds_partition(n, world):
+    seen = []
+    for r in range(world):
+        b, e = shard_bounds(n, world, r)
+        assert 0 <= b <= e <= n
+        seen.extend(range(b, e))
+    assert seen == list(range(n))
+    sizes = [shard_bounds(n, world, r)[1] - shard_bounds(n, world, r)[0] for r in range(world)]
+    assert max(sizes) - min(sizes) <= 1
