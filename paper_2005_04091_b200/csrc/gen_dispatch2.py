@@ -31,7 +31,7 @@ import os
 import sys
 
 # (R, T, S) variants instantiated by kernel_pipe.cu
-VARIANTS = [(4, 4, 8)]
+VARIANTS = [(4, 4, 8), (4, 8, 4)]
 
 
 def gen(R: int, T: int, S: int) -> str:

@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "spconv_internal.h"
@@ -110,17 +111,16 @@ __device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(uint3
 
 #include "dispatch2_gen.inc"
 
-// Fill stage s with input channel k (and the CTA's stream chunk of k).  TMA:
-// called by one lane.  cp.async: called by a whole warp.
+// Fill stage s with chunk k (channels [k*cc, k*cc + cc)) of the unit at (n0, iy0)
+// and the unit's stream chunk [c_beg, c_end).  TMA: called by one lane.
+// cp.async: called by a whole warp.
 template <int XS>
 __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeArgs &a, uint32_t smem0,
-                                           uint32_t fb, int s, int k, int n0, int iy0, const int32_t *cstart,
+                                           uint32_t fb, int s, int k, int n0, int iy0, int c_beg, int c_end,
                                            int lane) {
     const uint32_t stage_bytes = uint32_t(a.in_pad + a.st_bytes);
     const uint32_t dst_in = smem0 + uint32_t(s) * stage_bytes;
     const uint32_t dst_st = dst_in + uint32_t(a.in_pad);
-    // k = stage index: channels [k*cc, k*cc + cc)
-    const int c_beg = __ldg(cstart + k), c_end = __ldg(cstart + k + 1);
     const uint32_t st_bytes = uint32_t(c_end - c_beg);
     // order the consumers' generic-proxy reads of this stage before the async-proxy writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -150,6 +150,19 @@ __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeAr
     }
 }
 
+// A unit of work = (image group, block of tile rows, group set): decoded here.
+struct Unit {
+    int gs, n0, ty0;
+};
+__device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
+    Unit r;
+    r.gs = u % a.num_gsets;
+    u /= a.num_gsets;
+    r.ty0 = (u % a.blocks_y) * a.tr;
+    r.n0 = (u / a.blocks_y) * a.ipb;
+    return r;
+}
+
 template <int R, int PT, int PS, bool FUSED, int XS>
 __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
@@ -158,20 +171,27 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     __shared__ int done_cnt[MAXSTAGE];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int bid = blockIdx.x;
-    const int gs = bid % a.num_gsets;
-    bid /= a.num_gsets;
-    const int by = bid % a.blocks_y;
-    const int n0 = (bid / a.blocks_y) * a.ipb; // first image of the block
-    const int ty0 = by * a.tr;                 // first tile row of the block
-    const int nconsumers = min(a.gpc, a.num_groups - gs * a.gpc);
+    const int nwarps = blockDim.x >> 5;
     const int ns = a.nstage;
     const uint32_t stage_bytes = uint32_t(a.in_pad + a.st_bytes);
     const uint32_t smem0 = smem_u32(smem);
-    const int iy0 = ty0 * PT - 1; // first staged input row (pad = 1)
-    const int32_t *cstart = a.chunk_start + (size_t)gs * (a.nchunks + 1);
-    if (warp >= nconsumers) return; // whole warp exits before any barrier use
+    // chunk byte offsets of every group set, the group -> output channel table and
+    // the bias, copied once to shared memory (the epilogue must not wait on L2)
+    int32_t *s_cstart = reinterpret_cast<int32_t *>(smem + size_t(ns) * stage_bytes);
+    const int ncs = a.num_gsets * (a.nchunks + 1);
+    int32_t *s_rows = s_cstart + ncs;
+    float *s_bias = reinterpret_cast<float *>(s_rows + a.num_groups * R);
 
+    // persistent CTA: units blockIdx.x, blockIdx.x + gridDim.x, ...; stages are
+    // numbered across units so the ring prefetches the next unit's first channels
+    // while this unit finishes (and during its epilogue).
+    const int nunits = ((a.N + a.ipb - 1) / a.ipb) * a.blocks_y * a.num_gsets;
+    const int my_units = blockIdx.x < nunits ? (nunits - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int total = my_units * a.nchunks;
+
+    for (int i = threadIdx.x; i < ncs; i += blockDim.x) s_cstart[i] = __ldg(a.chunk_start + i);
+    for (int i = threadIdx.x; i < a.num_groups * R; i += blockDim.x) s_rows[i] = __ldg(a.group_rows + i);
+    for (int i = threadIdx.x; i < a.F; i += blockDim.x) s_bias[i] = __ldg(a.bias + i);
     if (threadIdx.x == 0) {
         for (int s = 0; s < ns; ++s) {
             mbar_init(smem_u32(&full_bar[s]), XS == 3 ? 1u : 33u);
@@ -179,88 +199,105 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
+    __syncthreads();
+
+    auto fill = [&](int kk) {
+        const int j = kk / a.nchunks, ch = kk - j * a.nchunks;
+        const Unit un = decode_unit(a, blockIdx.x + j * gridDim.x);
+        const int32_t *cs = s_cstart + un.gs * (a.nchunks + 1);
+        const int s = kk % ns;
+        fill_stage<XS>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, ch, un.n0, un.ty0 * PT - 1, cs[ch],
+                       cs[ch + 1], lane);
+    };
     if (warp == 0) {
-        // prologue: fill the first stages
-        for (int k = 0; k < min(ns, a.nchunks); ++k) {
+        for (int kk = 0; kk < min(ns, total); ++kk) {
             if (XS == 3 && lane != 0) continue;
-            fill_stage<XS>(&tmap, a, smem0, smem_u32(&full_bar[k]), k, k, n0, iy0, cstart, lane);
+            fill(kk);
         }
     }
-    // all consumer warps must see the initialised barriers (bar.sync over nconsumers warps)
-    asm volatile("bar.sync 1, %0;" ::"r"(nconsumers * 32) : "memory");
 
-    // ---------------- consumer warps ----------------
-    const int g = gs * a.gpc + warp;
     const int per_img_tiles = a.tr * a.tiles_x;
     const bool lane_ok = lane < a.lanes;
     const int li = lane_ok ? lane : 0;
     const int im = li / per_img_tiles;
     const int rem = li - im * per_img_tiles;
     const int tyl = rem / a.tiles_x, tx = rem - tyl * a.tiles_x;
-    // word offset of this thread's 6x6 window inside a stage (16-byte aligned)
+    // byte offset of this thread's window inside a stage (16-byte aligned)
     const uint32_t win_off = uint32_t((im * a.cc * a.rs + tyl * PT) * a.pitch + tx * PS) * 4u;
     const uint32_t row_bytes = uint32_t(a.pitch) * 4u;
     const uint32_t ch_bytes = uint32_t(a.rs * a.pitch) * 4u;
 
     constexpr int SH = PS / 2, PAIRS = (PS + 2) / 2;
-    uint64_t acc[R][PT][SH];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int t = 0; t < PT; ++t)
-#pragma unroll
-            for (int h = 0; h < SH; ++h) acc[r][t][h] = 0ull;
+    for (int j = 0; j < my_units; ++j) {
+        const Unit un = decode_unit(a, blockIdx.x + j * gridDim.x);
+        const int g = un.gs * a.gpc + warp;
+        const bool active = g < a.num_groups; // warp-uniform
 
-    for (int k = 0; k < a.nchunks; ++k) {
-        const int s = k % ns;
-        mbar_wait(smem_u32(&full_bar[s]), (k / ns) & 1);
-        const unsigned char *stage = smem + size_t(s) * stage_bytes;
-        const uint32_t st_base = smem0 + uint32_t(s) * stage_bytes + uint32_t(a.in_pad);
-        uint32_t sp = st_base + reinterpret_cast<const uint32_t *>(stage + a.in_pad)[warp];
-        uint32_t wp = smem0 + uint32_t(s) * stage_bytes + win_off; // window of the stage's first channel
-        uint64_t xw[PT + 2][PAIRS];
-        const unsigned char *wptr = stage + win_off;
+        uint64_t acc[R][PT][SH];
 #pragma unroll
-        for (int i = 0; i < PT + 2; ++i) {
+        for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int j = 0; j + 1 < PAIRS; j += 2) {
-                const ulonglong2 q = *reinterpret_cast<const ulonglong2 *>(wptr + i * row_bytes + 16 * (j / 2));
-                xw[i][j] = q.x;
-                xw[i][j + 1] = q.y;
+            for (int t = 0; t < PT; ++t)
+#pragma unroll
+                for (int h = 0; h < SH; ++h) acc[r][t][h] = 0ull;
+
+        for (int ch = 0; ch < a.nchunks; ++ch) {
+            const int kk = j * a.nchunks + ch;
+            const int s = kk % ns;
+            mbar_wait(smem_u32(&full_bar[s]), (kk / ns) & 1);
+            if (active) {
+                const unsigned char *stage = smem + size_t(s) * stage_bytes;
+                const uint32_t st_base = smem0 + uint32_t(s) * stage_bytes + uint32_t(a.in_pad);
+                uint32_t sp = st_base + reinterpret_cast<const uint32_t *>(stage + a.in_pad)[warp];
+                uint32_t wp = smem0 + uint32_t(s) * stage_bytes + win_off; // first channel's window
+                uint64_t xw[PT + 2][PAIRS];
+                const unsigned char *wptr = stage + win_off;
+#pragma unroll
+                for (int i = 0; i < PT + 2; ++i) {
+#pragma unroll
+                    for (int q = 0; q + 1 < PAIRS; q += 2) {
+                        const ulonglong2 v2 =
+                            *reinterpret_cast<const ulonglong2 *>(wptr + i * row_bytes + 16 * (q / 2));
+                        xw[i][q] = v2.x;
+                        xw[i][q + 1] = v2.y;
+                    }
+                    if constexpr (PAIRS % 2)
+                        xw[i][PAIRS - 1] =
+                            *reinterpret_cast<const uint64_t *>(wptr + i * row_bytes + 8 * (PAIRS - 1));
+                }
+                // one walk over the stage's channels: taps, "next channel" (window reload), end
+                if constexpr (R == 4 && PT == 4 && PS == 8) {
+                    SPC2_DISPATCH_R4T4S8(acc, xw, sp, wp, ch_bytes, row_bytes);
+                } else {
+                    static_assert(R == 4 && PT == 8 && PS == 4, "no dispatcher generated for this variant");
+                    SPC2_DISPATCH_R4T8S4(acc, xw, sp, wp, ch_bytes, row_bytes);
+                }
             }
-            if constexpr (PAIRS % 2)
-                xw[i][PAIRS - 1] = *reinterpret_cast<const uint64_t *>(wptr + i * row_bytes + 8 * (PAIRS - 1));
+            // release stage s: the last warp to finish with it refills it with stage kk + ns
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) {
+                // monotonic: the n-th use of stage s completes when the count reaches n*nwarps
+                const int old = atomicAdd(&done_cnt[s], 1);
+                last = (old % nwarps) == nwarps - 1;
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last && kk + ns < total) {
+                if (XS == 0 || lane == 0) fill(kk + ns);
+            }
         }
-        // one walk over the stage's channels: taps, "next channel" (window reload), end
-        static_assert(R == 4 && PT == 4 && PS == 8, "no dispatcher generated for this variant");
-        SPC2_DISPATCH_R4T4S8(acc, xw, sp, wp, ch_bytes, row_bytes);
+        if (!active) continue;
 
-        // release stage s: the last warp to finish with it refills it with channel k + ns
-        __syncwarp();
-        int last = 0;
-        if (lane == 0) {
-            // monotonic: the n-th use of stage s completes when the count reaches n*nconsumers
-            const int old = atomicAdd(&done_cnt[s], 1);
-            last = (old % nconsumers) == nconsumers - 1;
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last && k + ns < a.nchunks) {
-            if (XS == 0 || lane == 0)
-                fill_stage<XS>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, k + ns, n0, iy0, cstart, lane);
-        }
-    }
-
-    // ---------------- epilogue (a6) ----------------
-    const int n = n0 + im;
-    const int ty = ty0 + tyl;
-    const bool out_ok = lane_ok && n < a.N && ty < a.tiles_y;
-    const int oy0 = ty * PT, ox0 = tx * PS - XS;
+        // ---------------- epilogue (a6) ----------------
+        const int n = un.n0 + im;
+        const int ty = un.ty0 + tyl;
+        const bool out_ok = lane_ok && n < a.N && ty < a.tiles_y;
+        const int oy0 = ty * PT, ox0 = tx * PS - XS;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int f = __ldg(a.group_rows + g * R + r);
+        const int f = s_rows[g * R + r];
         if (f < 0) continue; // warp-uniform
-        const float b = __ldg(a.bias + f);
+        const float b = s_bias[f];
         float v[PT][PS];
 #pragma unroll
         for (int t = 0; t < PT; ++t)
@@ -335,6 +372,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
                 }
             }
         }
+    }
     }
 }
 
@@ -419,8 +457,14 @@ bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {
 void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g) {
     g = PipeGeometry{};
     g.xs = tma ? 3 : 0;
-    g.T = 4;
-    g.S = 8; // 4x8 tiles: 16 FFMA2 per nonzero (scripts/probes/dispatch_probe.cu)
+    // 32-pixel thread tiles: 16 FFMA2 per nonzero (scripts/probes/dispatch_probe.cu).
+    // 8x4 (tall) keeps the window's 128-bit loads at a 16-byte lane stride (no bank
+    // conflicts); 4x8 is the alternative (SPCONV_PIPE_TILE=4x8).
+    g.T = 8;
+    g.S = 4;
+    if (const char *e = std::getenv("SPCONV_PIPE_TILE")) {
+        if (std::strcmp(e, "4x8") == 0) { g.T = 4; g.S = 8; }
+    }
     const int PT = g.T, PS = g.S;
     g.tiles_x = (p.Wo + g.xs + PS - 1) / PS;
     g.tiles_y = (p.Ho + PT - 1) / PT;
@@ -454,10 +498,11 @@ void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g) {
     g.in_pad = (g.in_words * 4 + 127) & ~127;
     g.st_bytes = (p.max_chunk_bytes + 32 + 127) & ~127; // + 2 entries of look-ahead slack
     const int stage_bytes = g.in_pad + g.st_bytes;
-    const int budget = 200 * 1024;
+    const int cstart_bytes = ((p.num_gsets * (g.nchunks + 1) + p.num_groups * p.R + p.F) * 4 + 15) & ~15;
+    const int budget = 220 * 1024 - cstart_bytes;
     g.nstage = std::min(MAXSTAGE, budget / stage_bytes);
     if (g.nstage < 2) return;
-    g.smem_bytes = size_t(g.nstage) * stage_bytes;
+    g.smem_bytes = size_t(g.nstage) * stage_bytes + cstart_bytes;
     g.ok = true;
 }
 
@@ -478,8 +523,18 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.cc = g.cc; a.nchunks = g.nchunks;
     a.gpc = p.gpc; a.num_groups = p.num_groups; a.num_gsets = p.num_gsets;
     a.tma = use_tma ? 1 : 0;
-    const int64_t grid64 = (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y * p.num_gsets;
-    if (grid64 > 0x7fffffff) return cudaErrorInvalidConfiguration;
+    const int64_t nunits = (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y * p.num_gsets;
+    if (nunits > 0x7fffffff) return cudaErrorInvalidConfiguration;
+    // persistent: one CTA per SM (the register file holds one 8-warp CTA)
+    static int sm_count[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!sm_count[dev & 63]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sm_count[dev & 63] = v;
+    }
+    const int64_t grid64 = std::min<int64_t>(nunits, sm_count[dev & 63]);
 
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
@@ -503,6 +558,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
                      : launch_one<RR, TT, SS, false, 0>(map, a, grid, g.smem_bytes, s);             \
     }
     SPC_PIPE_LAUNCH(4, 4, 8)
+    SPC_PIPE_LAUNCH(4, 8, 4)
 #undef SPC_PIPE_LAUNCH
     return cudaErrorInvalidValue;
 }

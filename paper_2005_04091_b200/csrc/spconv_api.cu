@@ -182,13 +182,14 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                 }
             }
         }
-        // channels per stage: about 20 KB of staged input per stage
+        // channels per stage: about 40 KB of staged input per stage (fewer stage
+        // boundaries: each costs a barrier wait, a header load and a refill)
         p->pipe_cc = 1;
         p->max_chunk_bytes = 0;
         spconv::pipe_geometry(*p, false, p->pipe_cp);
         spconv::pipe_geometry(*p, true, p->pipe_tma);
         const int per_ch = std::max(p->pipe_tma.in_words, p->pipe_cp.in_words) * 4;
-        p->pipe_cc = std::max(1, std::min({8, C, 20480 / std::max(per_ch, 1)}));
+        p->pipe_cc = std::max(1, std::min({8, C, 40960 / std::max(per_ch, 1)}));
         const int cc = p->pipe_cc, nchunks = (C + cc - 1) / cc;
         const uint32_t NEXT = uint32_t(R * 9), END = uint32_t(R * 9 + 1);
         std::vector<int32_t> cstart(size_t(p->num_gsets) * (nchunks + 1));
