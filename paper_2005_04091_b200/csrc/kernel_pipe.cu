@@ -448,10 +448,11 @@ int window_wavefronts(const PipeGeometry &g, int pitch) {
 
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     (void)C; (void)F; (void)H;
-    // 4x8 tiles, whole tile rows per block: at most 32 tiles across.  AUTO uses this
+    // 32-pixel tiles, whole tile rows per block: at most 32 tiles across.  AUTO uses this
     // kernel only where TMA can stage the input (16-byte row stride); the cp.async
     // fallback inside it remains for misaligned input pointers.
-    return K == 3 && stride == 1 && pad == 1 && W + 3 <= 8 * 32 && (W * 4) % 16 == 0;
+    // (8x4 tiles: Wo + 3 <= 4 * 32)
+    return K == 3 && stride == 1 && pad == 1 && W + 3 <= 4 * 32 && (W * 4) % 16 == 0;
 }
 
 void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g) {

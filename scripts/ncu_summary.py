@@ -13,6 +13,7 @@ import argparse
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -109,6 +110,8 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--config", default="")
     ap.add_argument("--flops", type=float)
+    ap.add_argument("--traffic-json", help="merge {config: {kernel, dram_bytes_per_launch}} into this file")
+    ap.add_argument("--kernel-name", default="pipe", help="library kernel name recorded with the traffic")
     a = ap.parse_args()
     s = {"report": a.report, "config": a.config, "kernels": summarise(a.report, a.flops)}
     if a.launches:
@@ -133,6 +136,17 @@ def main():
             for k, v in s["launch_list"].items():
                 f.write(f"  {v['launches']:4d} x {v['mean_ns'] / 1e3:9.2f} us  share {v['share']:.3f}  {k}\n")
     print(open(a.out + ".txt").read())
+    if a.traffic_json and s["kernels"] and "dram_bytes_per_launch" in s["kernels"][0]:
+        try:
+            with open(a.traffic_json) as f:
+                t = json.load(f)
+        except (OSError, ValueError):
+            t = {}
+        t[a.config] = {"kernel": a.kernel_name,
+                       "dram_bytes_per_launch": int(s["kernels"][0]["dram_bytes_per_launch"]),
+                       "source": os.path.basename(a.out) + ".txt"}
+        with open(a.traffic_json, "w") as f:
+            json.dump(t, f, indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":

@@ -7,10 +7,10 @@
 #include <cstdlib>
 #include <vector>
 #include "../../paper_2005_04091_b200/csrc/dispatch2_gen.inc"
-#include "probe_bra.inc"
+#include "probe_variants.inc"
 
-template <int R, int T, int S, int MINB, int BRA = 0>
-__global__ void __launch_bounds__(256, MINB) k(const uint4* stream, int len, int reps, float* out) {
+template <int R, int T, int S, int MINB, int BRA = 0, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) k(const uint4* stream, int len, int reps, float* out) {
   extern __shared__ uint4 sst[];
   for (int i = threadIdx.x; i < len + 2; i += blockDim.x) sst[i] = stream[i];
   __syncthreads();
@@ -29,14 +29,15 @@ __global__ void __launch_bounds__(256, MINB) k(const uint4* stream, int len, int
   for (int rep = 0; rep < reps; ++rep) {
     uint32_t sp = (uint32_t)__cvta_generic_to_shared(sst);
     uint32_t wp = (uint32_t)__cvta_generic_to_shared(win);
-    if constexpr (BRA) { PROBE_BRA_R4T4S8(acc, xw, sp, wp, 0u, 48u); }
+    if constexpr (R == 2) { SPC2_DISPATCH_R2T8S4(acc, xw, sp, wp, 0u, 48u); }
+    else if constexpr (T == 8) { SPC2_DISPATCH_R4T8S4(acc, xw, sp, wp, 0u, 48u); }
     else { SPC2_DISPATCH_R4T4S8(acc, xw, sp, wp, 0u, 48u); }
   }
   float s = 0; for (int r = 0; r < R; ++r) for (int t = 0; t < T; ++t) for (int h = 0; h < SH; ++h) s += __uint_as_float((uint32_t)acc[r][t][h]);
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
-template <int R, int T, int S, int MINB = 1, int BRA = 0> void run(int blocks, int kx1, int mode = 0) {
+template <int R, int T, int S, int MINB = 1, int BRA = 0, int NT = 256> void run(int blocks, int kx1, int mode = 0) {
   const int len = 2000, reps = 200;
   std::vector<uint4> h(len + 2);
   srand(1);
@@ -51,23 +52,26 @@ template <int R, int T, int S, int MINB = 1, int BRA = 0> void run(int blocks, i
   }
   h[len] = make_uint4(0, 0, R * 9 + 1, 0); h[len + 1] = h[len];
   uint4* d; cudaMalloc(&d, h.size() * 16); cudaMemcpy(d, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
-  float* out; cudaMalloc(&out, blocks * 256 * 4);
+  float* out; cudaMalloc(&out, blocks * NT * 4);
   size_t smem = h.size() * 16;
-  cudaFuncSetAttribute(k<R, T, S, MINB, BRA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<R, T, S, MINB, BRA><<<blocks, 256, smem>>>(d, len, 2, out);
+  cudaFuncSetAttribute(k<R, T, S, MINB, BRA, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<R, T, S, MINB, BRA, NT><<<blocks, NT, smem>>>(d, len, 2, out);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   cudaEventRecord(a);
-  k<R, T, S, MINB, BRA><<<blocks, 256, smem>>>(d, len, reps, out);
+  k<R, T, S, MINB, BRA, NT><<<blocks, NT, smem>>>(d, len, reps, out);
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
-  double fl = 2.0 * T * S * (double)len * reps * blocks * 256;
+  double fl = 2.0 * T * S * (double)len * reps * blocks * NT;
   printf("bra=%d mode=%d R=%d T=%d S=%d kx1=%d blocks=%d: %.3f ms  %.1f TFLOP/s (%.0f%% of 74.4)  %s\n", BRA, mode, R, T, S, kx1, blocks, ms,
          fl / ms / 1e9, fl / ms / 1e9 / 74.4 * 100, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d); cudaFree(out);
 }
 
 int main() {
-  run<4, 4, 8, 1, 0>(148, 0, 0);
-  run<4, 4, 8, 1, 0>(148, 0, 1);
-  run<4, 4, 8, 1, 1>(148, 0, 1);
+  run<4, 4, 8, 1, 0, 256>(148, 1, 0);
+  run<4, 8, 4, 1, 0, 256>(148, 1, 0);
+  run<2, 8, 4, 1, 0, 384>(148, 1, 0);
+  run<2, 8, 4, 1, 0, 256>(148, 1, 0);
+  run<4, 8, 4, 1, 0, 256>(148, 1, 1);
+  run<2, 8, 4, 1, 0, 384>(148, 1, 1);
 }

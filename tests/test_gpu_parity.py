@@ -166,6 +166,14 @@ EDGE = [
     (1, 4, 6, 6, 4, 3, 1, 0, 0.5, "generic"),    # valid conv (pad 0)
     (1, 4, 6, 6, 4, 3, 1, 1, 0.0, "tiled"),      # nnz = 0 -> bias
     (1, 4, 6, 6, 4, 3, 1, 1, 0.0, "generic"),
+    # pipelined kernel (TMA staging needs W % 4 == 0)
+    (3, 5, 13, 12, 9, 3, 1, 1, 0.3, "pipe"),     # F not a multiple of R (3 warps), odd H
+    (1, 17, 6, 40, 12, 3, 1, 1, 0.15, "pipe"),   # C not a multiple of the channels per stage
+    (5, 4, 4, 4, 4, 3, 1, 1, 0.5, "pipe"),       # several images per block, N not a multiple
+    (2, 7, 9, 20, 5, 3, 1, 1, 1.0, "pipe"),      # dense
+    (1, 4, 6, 8, 4, 3, 1, 1, 0.0, "pipe"),       # nnz = 0 -> bias
+    (2, 3, 10, 124, 40, 3, 1, 1, 0.2, "pipe"),   # widest supported row (32 tiles), 2 group sets
+    (1, 2, 3, 4, 1, 3, 1, 1, 0.6, "pipe"),       # F = 1
 ]
 
 
@@ -178,7 +186,7 @@ def test_edge_cases(case):
     b = synthgen.make_bias(F, seed + 3)
     from paper_2005_04091_b200 import SparseConv2d
     layer = SparseConv2d(C, H, W, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b, kernel=kernel)
-    assert layer.info["kernel"] == (2 if kernel == "tiled" else 1)
+    assert layer.info["kernel"] == {"generic": 1, "tiled": 2, "pipe": 3}[kernel]
     x = torch.from_numpy(xh).cuda()
     y = layer(x).cpu().numpy()
     ref = oracle.conv_f32(xh, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b)
@@ -191,11 +199,12 @@ def test_edge_cases(case):
     layer.close()
 
 
-def test_unaligned_input_uses_cp_async_path():
+@pytest.mark.parametrize("kernel", ["tiled", "pipe"])
+def test_unaligned_input_uses_cp_async_path(kernel):
     cfg = synthgen.CONFIGS["c2"].with_batch(1)
     L = synthgen.make_layer(cfg)
     c = L.csr
-    layer = _layer(cfg, c, None, "tiled")
+    layer = _layer(cfg, c, None, kernel)
     buf = torch.empty(L.x.size + 1, dtype=torch.float32, device="cuda")
     x = buf[1:].view(L.x.shape)  # 4-byte aligned, not 16-byte aligned
     x.copy_(torch.from_numpy(L.x))
