@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round evidence pass on one B200: GPU tests, smoke, the default bench line (c2),
+# bench lines for every config, the reference arm, the ncu launch list of the
+# default bench command and one `ncu --set full` capture per headline config.
+set -u
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+: > gpurun_out/bench_all.jsonl
+for c in c1 c2 c3 c4_50 c4_80 c4_90 c4_95 c5; do
+  timeout 600 python bench.py --config $c --steps 200 --warmup 5 --no-cpu-baseline >> gpurun_out/bench_all.jsonl 2>> gpurun_out/bench_all.err
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 200 --csv \
+   --log-file gpurun_out/launches_c2.csv python bench.py --steps 300 --warmup 20 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
+for c in c2 c3 c5; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pipe_kernel -s 3 -c 1 \
+     -o gpurun_out/full_$c -f python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/full_$c.log 2>&1
+done
+echo done
