@@ -32,6 +32,7 @@ import sys
 
 # (R, T, S) variants instantiated by kernel_pipe.cu
 VARIANTS = [(4, 4, 8), (4, 8, 4)]
+MASK_VARIANTS = [(4, 8, 4)]
 
 
 def gen(R: int, T: int, S: int) -> str:
@@ -121,11 +122,117 @@ def gen(R: int, T: int, S: int) -> str:
             f"                 : \"memory\")\n")
 
 
+def gen_mask(R: int, T: int, S: int) -> str:
+    """Mask walk for one channel (the default dispatcher, see kernel_pipe.cu).
+
+    Operands: accumulator pairs (in/out), window pairs (in), the channel's 9R-bit
+    tap x row mask (in), the smem address of the channel's DENSE value block (9R
+    (v, v) pairs, zeros for absent taps; in) and the tap-0 values already loaded
+    (R pairs, in/out: on exit they hold the NEXT channel's tap-0 values).
+
+    Straight-line code over the 9R (tap, row) blocks in tap-major, row-minor
+    order.  The values of tap t+1 are requested at the top of tap t into the other
+    of two register sets (tap parity is static, so no copies); a tap with no row is
+    skipped with one branch, a row without the tap with one more.  Branch
+    conditions go through vote.sync so ptxas knows they are warp-uniform.
+    """
+    PAIRS = (S + 2) // 2
+    SH = S // 2
+    nacc = R * T * SH
+
+    def A(r, t, h):
+        return f"%{(r * T + t) * SH + h}"
+
+    V0 = nacc              # first of R in/out value pairs (tap-0 set)
+    XB = nacc + R
+
+    def X(i, j):
+        return f"%{XB + i * PAIRS + j}"
+
+    M = f"%{XB + (T + 2) * PAIRS}"      # 64-bit mask (in)
+    VB = f"%{XB + (T + 2) * PAIRS + 1}"  # u32 smem address of the dense values (in)
+    tag = f"M{R}T{T}S{S}"
+    # value registers: set 0 = the in/out operands, set 1 = locals
+    def VAL(tap, r):
+        return f"%{V0 + r}" if tap % 2 == 0 else f"%%w{r}"
+
+    L = ["{", ".reg .pred %%p, %%q;", ".reg .b64 " + ", ".join(f"%%w{r}" for r in range(R)) + ";",
+         ".reg .b32 %%mlo, %%mhi, %%mw, %%bt;",
+         ".reg .f32 %%v1, %%vd, " + ", ".join(f"%%a{i}" for i in range(S)) + ", "
+         + ", ".join(f"%%x{i}" for i in range(S + 2)) + ";",
+         f"mov.b64 {{%%mlo, %%mhi}}, {M};"]
+
+    def load_tap(tap):  # values of `tap` into its set (tap 9 = next channel's tap 0)
+        out = []
+        off = tap * R * 8
+        regs = [VAL(tap, r) for r in range(R)]
+        for r in range(0, R, 2):
+            out.append(f"ld.shared.v2.b64 {{{regs[r]}, {regs[r + 1]}}}, [{VB}+{off + 8 * r}];")
+        return out
+
+    for tap in range(9):
+        ky, kx = tap // 3, tap % 3
+        L += load_tap(tap + 1)   # prefetch the next tap's values (tap 9 -> next channel's tap 0)
+        lo_bit = tap * R
+        if lo_bit + R <= 32:
+            word, sh = "%%mlo", lo_bit
+        elif lo_bit >= 32:
+            word, sh = "%%mhi", lo_bit - 32
+        else:
+            word, sh = None, 0
+        if word is not None:
+            L.append(f"and.b32 %%mw, {word}, {((1 << R) - 1) << sh};")
+        else:
+            L.append(f"shf.r.clamp.b32 %%mw, %%mlo, %%mhi, {lo_bit};")
+            L.append(f"and.b32 %%mw, %%mw, {(1 << R) - 1};")
+        L.append("setp.eq.u32 %%p, %%mw, 0;")
+        L.append(f"@%%p bra.uni $K{tag}_t{tap};")
+        for r in range(R):
+            L.append(f"and.b32 %%bt, %%mw, {1 << (sh + r)};")
+            L.append("setp.eq.u32 %%p, %%bt, 0;")
+            L.append(f"@%%p bra.uni $K{tag}_t{tap}r{r};")
+            v = VAL(tap, r)
+            if kx != 1:
+                for t in range(T):
+                    for h in range(SH):
+                        L.append(f"fma.rn.f32x2 {A(r, t, h)}, {v}, {X(t + ky, h + kx // 2)}, {A(r, t, h)};")
+            else:
+                L.append(f"mov.b64 {{%%v1, %%vd}}, {v};")
+                for t in range(T):
+                    row = t + ky
+                    for j in range(PAIRS):
+                        L.append(f"mov.b64 {{%%x{2 * j}, %%x{2 * j + 1}}}, {X(row, j)};")
+                    for h in range(SH):
+                        L.append(f"mov.b64 {{%%a{2 * h}, %%a{2 * h + 1}}}, {A(r, t, h)};")
+                    for s_ in range(S):
+                        L.append(f"fma.rn.f32 %%a{s_}, %%v1, %%x{s_ + 1}, %%a{s_};")
+                    for h in range(SH):
+                        L.append(f"mov.b64 {A(r, t, h)}, {{%%a{2 * h}, %%a{2 * h + 1}}};")
+            L.append(f"$K{tag}_t{tap}r{r}:")
+        L.append(f"$K{tag}_t{tap}:")
+    # tap 9 (odd) loaded into %%w: hand the next channel's tap-0 values back in set 0
+    for r in range(R):
+        L.append(f"mov.b64 %{V0 + r}, %%w{r};")
+    L.append("}")
+    asm = "\\n\\t".join(L)
+    outs = ", ".join(f'"+l"(acc[{r}][{t}][{h}])' for r in range(R) for t in range(T) for h in range(SH))
+    vals = ", ".join(f'"+l"(v0[{r}])' for r in range(R))
+    ins = ", ".join(f'"l"(xw[{i}][{j}])' for i in range(T + 2) for j in range(PAIRS))
+    return (f"#define SPC2_MASKWALK_{tag}(acc, v0, xw, m, vb) \\\n"
+            f"    asm volatile(\"{asm}\" \\\n"
+            f"                 : {outs}, {vals} \\\n"
+            f"                 : {ins}, \"l\"(m), \"r\"(vb) \\\n"
+            f"                 : \"memory\")\n")
+
+
 def main(out_path: str) -> None:
     text = ["// GENERATED by gen_dispatch2.py — do not edit.\n"]
     for R, T, S in VARIANTS:
         text.append(f"// R={R} rows, thread tile T={T} x S={S}, window {T + 2} x {S + 2} as 64-bit pairs.\n")
         text.append(gen(R, T, S))
+    for R, T, S in MASK_VARIANTS:
+        text.append(f"// mask walk: R={R} rows, thread tile T={T} x S={S}.\n")
+        text.append(gen_mask(R, T, S))
     tmp = out_path + ".tmp"
     with open(tmp, "w") as f:
         f.write("\n".join(text))

@@ -111,6 +111,53 @@ __device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(uint3
 
 #include "dispatch2_gen.inc"
 
+// Mask dispatcher (SPCONV_PIPE_DISPATCH=mask; the brx.idx walk is the default,
+// measured faster on B200 -- DESIGN.md §7): per (row group, channel) the stream holds a 9*R-bit
+// mask (bit tap*R + r: row r of the group has a nonzero at tap = ky*3 + kx) and a
+// dense block of 9*R (v, v) value pairs (zero where the mask bit is clear).  The
+// walk (SPC2_MASKWALK_*, gen_dispatch2.py) is straight-line code over the 9*R
+// (tap, row) blocks with warp-uniform forward skips: no indirect branch and no
+// jump-table load per nonzero, and the values of tap t+1 are loaded at static
+// offsets while tap t runs.  Within a row the taps are consumed in ascending
+// (ky, kx) order and channels ascend, i.e. ascending colidx (the FP32 contract;
+// a skipped tap contributes exactly nothing, as fma(0, x, acc) == acc).
+// Segment layout per (warp, stage): the ncl masks (16-byte padded), then the ncl
+// dense value blocks back to back.
+template <int R, int PT, int PS>
+__device__ __forceinline__ void mask_walk(uint64_t (&acc)[R][PT][PS / 2], const unsigned char *wbase,
+                                          const unsigned char *seg, uint32_t seg_s, int ncl, uint32_t row_bytes,
+                                          uint32_t ch_bytes) {
+    constexpr int PAIRS = (PS + 2) / 2;
+    const uint64_t *masks = reinterpret_cast<const uint64_t *>(seg);
+    const uint32_t dense0 = uint32_t((ncl * 8 + 15) & ~15); // dense value blocks start 16-byte aligned
+    uint32_t vb = seg_s + dense0;
+    uint64_t v0[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v0[r] = *reinterpret_cast<const uint64_t *>(seg + dense0 + 8 * r);
+#pragma unroll 1
+    for (int cl = 0; cl < ncl; ++cl) {
+        uint64_t xw[PT + 2][PAIRS];
+        const unsigned char *wptr = wbase + cl * ch_bytes;
+#pragma unroll
+        for (int i = 0; i < PT + 2; ++i) {
+#pragma unroll
+            for (int q = 0; q + 1 < PAIRS; q += 2) {
+                const ulonglong2 v2 = *reinterpret_cast<const ulonglong2 *>(wptr + i * row_bytes + 16 * (q / 2));
+                xw[i][q] = v2.x;
+                xw[i][q + 1] = v2.y;
+            }
+            if constexpr (PAIRS % 2)
+                xw[i][PAIRS - 1] = *reinterpret_cast<const uint64_t *>(wptr + i * row_bytes + 8 * (PAIRS - 1));
+        }
+        // broadcast from lane 0 so ptxas can prove the mask (and every branch on it)
+        // warp-uniform: uniform branches need no convergence barriers
+        const uint64_t m = __shfl_sync(0xffffffffu, masks[cl], 0);
+        static_assert(R == 4 && PT == 8 && PS == 4, "no mask walk generated for this variant");
+        SPC2_MASKWALK_M4T8S4(acc, v0, xw, m, vb);
+        vb += 9u * R * 8u;
+    }
+}
+
 // Fill stage s with chunk k (channels [k*cc, k*cc + cc)) of the unit at (n0, iy0)
 // and the unit's stream chunk [c_beg, c_end).  TMA: called by one lane.
 // cp.async: called by a whole warp.
@@ -163,7 +210,7 @@ __device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
     return r;
 }
 
-template <int R, int PT, int PS, bool FUSED, int XS>
+template <int R, int PT, int PS, bool FUSED, int XS, int DISP>
 __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -248,7 +295,13 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
             if (active) {
                 const unsigned char *stage = smem + size_t(s) * stage_bytes;
                 const uint32_t st_base = smem0 + uint32_t(s) * stage_bytes + uint32_t(a.in_pad);
-                uint32_t sp = st_base + reinterpret_cast<const uint32_t *>(stage + a.in_pad)[warp];
+                const uint32_t seg_off = reinterpret_cast<const uint32_t *>(stage + a.in_pad)[warp];
+                if constexpr (DISP == 1) {
+                    const int ncl = min(a.cc, a.C - ch * a.cc);
+                    mask_walk<R, PT, PS>(acc, stage + win_off, stage + a.in_pad + seg_off, st_base + seg_off, ncl,
+                                         row_bytes, ch_bytes);
+                } else {
+                uint32_t sp = st_base + seg_off;
                 uint32_t wp = smem0 + uint32_t(s) * stage_bytes + win_off; // first channel's window
                 uint64_t xw[PT + 2][PAIRS];
                 const unsigned char *wptr = stage + win_off;
@@ -271,6 +324,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
                 } else {
                     static_assert(R == 4 && PT == 8 && PS == 4, "no dispatcher generated for this variant");
                     SPC2_DISPATCH_R4T8S4(acc, xw, sp, wp, ch_bytes, row_bytes);
+                }
                 }
             }
             // release stage s: the last warp to finish with it refills it with stage kk + ns
@@ -390,9 +444,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int R, int PT, int PS, bool FUSED, int XS>
+template <int R, int PT, int PS, bool FUSED, int XS, int DISP>
 cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = pipe_kernel<R, PT, PS, FUSED, XS>;
+    auto kern = pipe_kernel<R, PT, PS, FUSED, XS, DISP>;
     static size_t attr_done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -551,15 +605,15 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
     const int grid = int(grid64);
-#define SPC_PIPE_LAUNCH(RR, TT, SS)                                                                 \
-    if (p.R == RR && g.T == TT && g.S == SS) {                                                      \
-        if (use_tma) return fused ? launch_one<RR, TT, SS, true, 3>(map, a, grid, g.smem_bytes, s)  \
-                                  : launch_one<RR, TT, SS, false, 3>(map, a, grid, g.smem_bytes, s); \
-        return fused ? launch_one<RR, TT, SS, true, 0>(map, a, grid, g.smem_bytes, s)               \
-                     : launch_one<RR, TT, SS, false, 0>(map, a, grid, g.smem_bytes, s);             \
+#define SPC_PIPE_LAUNCH(RR, TT, SS, DD)                                                             \
+    if (p.R == RR && g.T == TT && g.S == SS && p.pipe_dispatch == DD) {                            \
+        if (use_tma) return fused ? launch_one<RR, TT, SS, true, 3, DD>(map, a, grid, g.smem_bytes, s)  \
+                                  : launch_one<RR, TT, SS, false, 3, DD>(map, a, grid, g.smem_bytes, s); \
+        return fused ? launch_one<RR, TT, SS, true, 0, DD>(map, a, grid, g.smem_bytes, s)               \
+                     : launch_one<RR, TT, SS, false, 0, DD>(map, a, grid, g.smem_bytes, s);             \
     }
-    SPC_PIPE_LAUNCH(4, 4, 8)
-    SPC_PIPE_LAUNCH(4, 8, 4)
+    SPC_PIPE_LAUNCH(4, 8, 4, 1)
+    SPC_PIPE_LAUNCH(4, 8, 4, 0)
 #undef SPC_PIPE_LAUNCH
     return cudaErrorInvalidValue;
 }

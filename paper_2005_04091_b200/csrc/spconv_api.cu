@@ -165,6 +165,10 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         // Ascending case within a channel, channels in order: every output row's
         // taps are consumed in ascending colidx order (the FP32 contract).
         p->gpc = std::min(p->num_groups, 8);
+        // brx.idx threaded code (default; measured faster on B200) or the tap-mask walk
+        p->pipe_dispatch = 0;
+        if (const char *e = std::getenv("SPCONV_PIPE_DISPATCH"))
+            if (std::strcmp(e, "mask") == 0) p->pipe_dispatch = 1;
         p->num_gsets = (p->num_groups + p->gpc - 1) / p->gpc;
         const int hdr = ((p->gpc * 4 + 15) / 16) * 16;
         std::vector<uint4> out;
@@ -204,6 +208,33 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                 for (int w = 0; w < p->gpc; ++w) {
                     const int g = gs * p->gpc + w;
                     offs[size_t(w)] = uint32_t((out.size() - base) * 16);
+                    if (p->pipe_dispatch == 1) {
+                        // mask walk: per channel a 9R-bit mask (bit tap*R + r) then the
+                        // values as (v, v) pairs in tap-major, row-minor order; 8-byte
+                        // items packed into the 16-byte stream words
+                        std::vector<uint64_t> items, dense;
+                        for (int c = c0; c < c1; ++c) {
+                            uint64_t m = 0;
+                            std::vector<uint64_t> blk(size_t(9 * R), 0);
+                            if (g < p->num_groups)
+                                for (auto &e : byc[size_t(g)][size_t(c)]) {
+                                    const int r = e.first / 9, tap = e.first % 9;
+                                    m |= uint64_t(1) << (tap * R + r);
+                                    uint32_t bits;
+                                    std::memcpy(&bits, &e.second, 4);
+                                    blk[size_t(tap * R + r)] = (uint64_t(bits) << 32) | bits;
+                                }
+                            items.push_back(m);
+                            dense.insert(dense.end(), blk.begin(), blk.end());
+                        }
+                        if (items.size() & 1) items.push_back(0); // dense blocks start 16-byte aligned
+                        items.insert(items.end(), dense.begin(), dense.end());
+                        if (items.size() & 1) items.push_back(0);
+                        for (size_t i = 0; i < items.size(); i += 2)
+                            out.push_back(make_uint4(uint32_t(items[i]), uint32_t(items[i] >> 32),
+                                                     uint32_t(items[i + 1]), uint32_t(items[i + 1] >> 32)));
+                        continue;
+                    }
                     for (int c = c0; c < c1; ++c) {
                         if (g < p->num_groups) {
                             auto v = byc[size_t(g)][size_t(c)];

@@ -83,6 +83,7 @@ struct Plan {
     int gpc = 0, num_gsets = 0;
     int max_chunk_bytes = 0;       // largest (gset, stage) stream chunk incl. header
     int pipe_cc = 1;               // input channels per pipeline stage
+    int pipe_dispatch = 0;         // 0: brx.idx threaded code (default), 1: tap-mask walk
     int32_t *d_chunk_start = nullptr; // [num_gsets * (nchunks + 1)] byte offsets into d_stream2
     uint4 *d_stream2 = nullptr;    // chunks: header (GPC u32 byte offsets) + 16-byte entries
     PipeGeometry pipe_tma{}, pipe_cp{};

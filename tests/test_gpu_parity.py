@@ -321,3 +321,12 @@ def test_concurrent_streams():
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o.view(torch.int32), ref.view(torch.int32))
+
+
+@pytest.mark.parametrize("name,fused", [("c2", False), ("c3", True), ("c5", False)])
+def test_pipe_mask_dispatcher(name, fused, monkeypatch):
+    """The alternative tap-mask walk of the pipelined kernel (SPCONV_PIPE_DISPATCH=mask)
+    obeys the same bitwise contract."""
+    monkeypatch.setenv("SPCONV_PIPE_DISPATCH", "mask")
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=1 if name == "c5" else 2)
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=1, integer=True)
