@@ -74,7 +74,8 @@ def gen(R: int, T: int, S: int) -> str:
     L.append(f"$D{tag}_T: .branchtargets " + ", ".join(f"$D{tag}_{i}" for i in range(ncase + 2)) + ";")
     L.append(f"brx.idx.uni %%cn, $D{tag}_T;")
     for i in range(ncase):
-        r, ky, kx = i // 9, (i // 3) % 3, i % 3
+        # tap-major case numbering: case = (ky*3 + kx)*R + r
+        r, ky, kx = i % R, (i // R) // 3, (i // R) % 3
         L.append(f"$D{tag}_{i}:")
         L.append("cvt.u32.u64 %%cn, %%kb;")  # case of entry k+1 (loaded one case ago)
         if kx != 1:

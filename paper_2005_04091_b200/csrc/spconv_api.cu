@@ -182,7 +182,7 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                 for (int32_t j = rowptr[f]; j < rowptr[f + 1]; ++j) {
                     const int col = colidx[size_t(j)];
                     const int c = col / 9, ky = (col / 3) % 3, kx = col % 3;
-                    byc[size_t(g)][size_t(c)].push_back({r * 9 + ky * 3 + kx, values[size_t(j)]});
+                    byc[size_t(g)][size_t(c)].push_back({(ky * 3 + kx) * R + r, values[size_t(j)]});
                 }
             }
         }
@@ -218,7 +218,7 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                             std::vector<uint64_t> blk(size_t(9 * R), 0);
                             if (g < p->num_groups)
                                 for (auto &e : byc[size_t(g)][size_t(c)]) {
-                                    const int r = e.first / 9, tap = e.first % 9;
+                                    const int r = e.first % R, tap = e.first / R;
                                     m |= uint64_t(1) << (tap * R + r);
                                     uint32_t bits;
                                     std::memcpy(&bits, &e.second, 4);
