@@ -186,83 +186,92 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                 }
             }
         }
-        // channels per stage: about 40 KB of staged input per stage (fewer stage
+        // channels per stage: about 80 KB of staged input per stage (fewer stage
         // boundaries: each costs a barrier wait, a header load and a refill)
         p->pipe_cc = 1;
         p->max_chunk_bytes = 0;
         spconv::pipe_geometry(*p, false, p->pipe_cp);
         spconv::pipe_geometry(*p, true, p->pipe_tma);
         const int per_ch = std::max(p->pipe_tma.in_words, p->pipe_cp.in_words) * 4;
-        p->pipe_cc = std::max(1, std::min({8, C, 40960 / std::max(per_ch, 1)}));
-        const int cc = p->pipe_cc, nchunks = (C + cc - 1) / cc;
-        const uint32_t NEXT = uint32_t(R * 9), END = uint32_t(R * 9 + 1);
-        std::vector<int32_t> cstart(size_t(p->num_gsets) * (nchunks + 1));
-        int maxb = 0;
-        for (int gs = 0; gs < p->num_gsets; ++gs) {
-            for (int j = 0; j < nchunks; ++j) {
-                const size_t base = out.size();
-                cstart[size_t(gs) * (nchunks + 1) + j] = int32_t(base * 16);
-                out.resize(base + size_t(hdr / 16));
-                std::vector<uint32_t> offs(size_t(p->gpc), 0);
-                const int c0 = j * cc, c1 = std::min(C, c0 + cc);
-                for (int w = 0; w < p->gpc; ++w) {
-                    const int g = gs * p->gpc + w;
-                    offs[size_t(w)] = uint32_t((out.size() - base) * 16);
-                    if (p->pipe_dispatch == 1) {
-                        // mask walk: per channel a 9R-bit mask (bit tap*R + r) then the
-                        // values as (v, v) pairs in tap-major, row-minor order; 8-byte
-                        // items packed into the 16-byte stream words
-                        std::vector<uint64_t> items, dense;
+        int stage_target = 81920; // measured best on B200
+        if (const char *e = std::getenv("SPCONV_PIPE_STAGE_BYTES")) stage_target = std::max(4096, std::atoi(e));
+        const bool tma_feasible = p->pipe_tma.ok;
+        std::vector<int32_t> cstart;
+        // the stream layout depends on cc; shrink cc until the ring fits shared memory
+        for (int cc_try = std::max(1, std::min({32, C, stage_target / std::max(per_ch, 1)}));; cc_try /= 2) {
+            p->pipe_cc = cc_try;
+            const int cc = p->pipe_cc, nchunks = (C + cc - 1) / cc;
+            out.clear();
+            const uint32_t NEXT = uint32_t(R * 9), END = uint32_t(R * 9 + 1);
+            cstart.assign(size_t(p->num_gsets) * (nchunks + 1), 0);
+            int maxb = 0;
+            for (int gs = 0; gs < p->num_gsets; ++gs) {
+                for (int j = 0; j < nchunks; ++j) {
+                    const size_t base = out.size();
+                    cstart[size_t(gs) * (nchunks + 1) + j] = int32_t(base * 16);
+                    out.resize(base + size_t(hdr / 16));
+                    std::vector<uint32_t> offs(size_t(p->gpc), 0);
+                    const int c0 = j * cc, c1 = std::min(C, c0 + cc);
+                    for (int w = 0; w < p->gpc; ++w) {
+                        const int g = gs * p->gpc + w;
+                        offs[size_t(w)] = uint32_t((out.size() - base) * 16);
+                        if (p->pipe_dispatch == 1) {
+                            // mask walk: per channel a 9R-bit mask (bit tap*R + r) then the
+                            // values as (v, v) pairs in tap-major, row-minor order; 8-byte
+                            // items packed into the 16-byte stream words
+                            std::vector<uint64_t> items, dense;
+                            for (int c = c0; c < c1; ++c) {
+                                uint64_t m = 0;
+                                std::vector<uint64_t> blk(size_t(9 * R), 0);
+                                if (g < p->num_groups)
+                                    for (auto &e : byc[size_t(g)][size_t(c)]) {
+                                        const int r = e.first % R, tap = e.first / R;
+                                        m |= uint64_t(1) << (tap * R + r);
+                                        uint32_t bits;
+                                        std::memcpy(&bits, &e.second, 4);
+                                        blk[size_t(tap * R + r)] = (uint64_t(bits) << 32) | bits;
+                                    }
+                                items.push_back(m);
+                                dense.insert(dense.end(), blk.begin(), blk.end());
+                            }
+                            if (items.size() & 1) items.push_back(0); // dense blocks start 16-byte aligned
+                            items.insert(items.end(), dense.begin(), dense.end());
+                            if (items.size() & 1) items.push_back(0);
+                            for (size_t i = 0; i < items.size(); i += 2)
+                                out.push_back(make_uint4(uint32_t(items[i]), uint32_t(items[i] >> 32),
+                                                         uint32_t(items[i + 1]), uint32_t(items[i + 1] >> 32)));
+                            continue;
+                        }
                         for (int c = c0; c < c1; ++c) {
-                            uint64_t m = 0;
-                            std::vector<uint64_t> blk(size_t(9 * R), 0);
-                            if (g < p->num_groups)
-                                for (auto &e : byc[size_t(g)][size_t(c)]) {
-                                    const int r = e.first % R, tap = e.first / R;
-                                    m |= uint64_t(1) << (tap * R + r);
+                            if (g < p->num_groups) {
+                                auto v = byc[size_t(g)][size_t(c)];
+                                std::stable_sort(v.begin(), v.end(),
+                                                 [](const std::pair<int, float> &a, const std::pair<int, float> &b) {
+                                                     return a.first < b.first;
+                                                 });
+                                for (auto &e : v) {
                                     uint32_t bits;
                                     std::memcpy(&bits, &e.second, 4);
-                                    blk[size_t(tap * R + r)] = (uint64_t(bits) << 32) | bits;
+                                    out.push_back(make_uint4(bits, bits, uint32_t(e.first), 0u));
                                 }
-                            items.push_back(m);
-                            dense.insert(dense.end(), blk.begin(), blk.end());
-                        }
-                        if (items.size() & 1) items.push_back(0); // dense blocks start 16-byte aligned
-                        items.insert(items.end(), dense.begin(), dense.end());
-                        if (items.size() & 1) items.push_back(0);
-                        for (size_t i = 0; i < items.size(); i += 2)
-                            out.push_back(make_uint4(uint32_t(items[i]), uint32_t(items[i] >> 32),
-                                                     uint32_t(items[i + 1]), uint32_t(items[i + 1] >> 32)));
-                        continue;
-                    }
-                    for (int c = c0; c < c1; ++c) {
-                        if (g < p->num_groups) {
-                            auto v = byc[size_t(g)][size_t(c)];
-                            std::stable_sort(v.begin(), v.end(),
-                                             [](const std::pair<int, float> &a, const std::pair<int, float> &b) {
-                                                 return a.first < b.first;
-                                             });
-                            for (auto &e : v) {
-                                uint32_t bits;
-                                std::memcpy(&bits, &e.second, 4);
-                                out.push_back(make_uint4(bits, bits, uint32_t(e.first), 0u));
                             }
+                            out.push_back(make_uint4(0u, 0u, c + 1 < c1 ? NEXT : END, 0u));
                         }
-                        out.push_back(make_uint4(0u, 0u, c + 1 < c1 ? NEXT : END, 0u));
                     }
+                    std::memcpy(reinterpret_cast<char *>(out.data() + base), offs.data(), offs.size() * 4);
+                    maxb = std::max(maxb, int((out.size() - base) * 16));
                 }
-                std::memcpy(reinterpret_cast<char *>(out.data() + base), offs.data(), offs.size() * 4);
-                maxb = std::max(maxb, int((out.size() - base) * 16));
+                cstart[size_t(gs) * (nchunks + 1) + nchunks] = int32_t(out.size() * 16);
             }
-            cstart[size_t(gs) * (nchunks + 1) + nchunks] = int32_t(out.size() * 16);
+            if (out.size() * 16 > size_t(INT32_MAX)) return SPCONV_ERR_UNSUPPORTED;
+            p->max_chunk_bytes = maxb;
+            spconv::pipe_geometry(*p, true, p->pipe_tma);
+            spconv::pipe_geometry(*p, false, p->pipe_cp);
+            if ((p->pipe_cp.ok && (p->pipe_tma.ok || !tma_feasible)) || cc_try == 1) break;
         }
-        if (out.size() * 16 > size_t(INT32_MAX)) return SPCONV_ERR_UNSUPPORTED;
-        p->max_chunk_bytes = maxb;
         if ((st = upload(&p->d_group_rows, grows.data(), grows.size(), p->device_bytes))) return st;
         if ((st = upload(&p->d_chunk_start, cstart.data(), cstart.size(), p->device_bytes))) return st;
         if ((st = upload(&p->d_stream2, out.data(), out.size(), p->device_bytes))) return st;
-        spconv::pipe_geometry(*p, true, p->pipe_tma);
-        spconv::pipe_geometry(*p, false, p->pipe_cp);
         if (!p->pipe_cp.ok) return SPCONV_ERR_UNSUPPORTED;
         return SPCONV_OK;
     }
