@@ -161,7 +161,7 @@ __device__ __forceinline__ void mask_walk(uint64_t (&acc)[R][PT][PS / 2], const 
 // Fill stage s with chunk k (channels [k*cc, k*cc + cc)) of the unit at (n0, iy0)
 // and the unit's stream chunk [c_beg, c_end).  TMA: called by one lane.
 // cp.async: called by a whole warp.
-template <int XS>
+template <int XS, int STG>
 __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeArgs &a, uint32_t smem0,
                                            uint32_t fb, int s, int k, int n0, int iy0, int c_beg, int c_end,
                                            int lane) {
@@ -171,9 +171,11 @@ __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeAr
     const uint32_t st_bytes = uint32_t(c_end - c_beg);
     // order the consumers' generic-proxy reads of this stage before the async-proxy writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if constexpr (XS == 3) {
+    if constexpr (STG == 1) {
+        // TMA: XS == 3 loads the caller's tensor from ix = -4 (16-byte aligned start);
+        // XS == 0 loads the left-padded copy (column 0 = the zero pad) from column 0
         mbar_expect_tx(fb, uint32_t(a.in_words) * 4u + st_bytes);
-        tma_load_4d(tmap, fb, dst_in, -(XS + 1), iy0, k * a.cc, n0);
+        tma_load_4d(tmap, fb, dst_in, XS == 3 ? -4 : 0, iy0, k * a.cc, n0);
         bulk_load(dst_st, a.stream + c_beg, st_bytes, fb);
     } else {
         if (lane == 0) {
@@ -210,7 +212,7 @@ __device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
     return r;
 }
 
-template <int R, int PT, int PS, bool FUSED, int XS, int DISP>
+template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG>
 __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     for (int i = threadIdx.x; i < a.F; i += blockDim.x) s_bias[i] = __ldg(a.bias + i);
     if (threadIdx.x == 0) {
         for (int s = 0; s < ns; ++s) {
-            mbar_init(smem_u32(&full_bar[s]), XS == 3 ? 1u : 33u);
+            mbar_init(smem_u32(&full_bar[s]), STG == 1 ? 1u : 33u);
             done_cnt[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -253,12 +255,12 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         const Unit un = decode_unit(a, blockIdx.x + j * gridDim.x);
         const int32_t *cs = s_cstart + un.gs * (a.nchunks + 1);
         const int s = kk % ns;
-        fill_stage<XS>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, ch, un.n0, un.ty0 * PT - 1, cs[ch],
+        fill_stage<XS, STG>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, ch, un.n0, un.ty0 * PT - 1, cs[ch],
                        cs[ch + 1], lane);
     };
     if (warp == 0) {
         for (int kk = 0; kk < min(ns, total); ++kk) {
-            if (XS == 3 && lane != 0) continue;
+            if (STG == 1 && lane != 0) continue;
             fill(kk);
         }
     }
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
             }
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last && kk + ns < total) {
-                if (XS == 0 || lane == 0) fill(kk + ns);
+                if (STG == 0 || lane == 0) fill(kk + ns);
             }
         }
         if (!active) continue;
@@ -444,9 +446,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int R, int PT, int PS, bool FUSED, int XS, int DISP>
+template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG>
 cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = pipe_kernel<R, PT, PS, FUSED, XS, DISP>;
+    auto kern = pipe_kernel<R, PT, PS, FUSED, XS, DISP, STG>;
     static size_t attr_done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -502,16 +504,18 @@ int window_wavefronts(const PipeGeometry &g, int pitch) {
 
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     (void)C; (void)F; (void)H;
-    // 32-pixel tiles, whole tile rows per block: at most 32 tiles across.  AUTO uses this
-    // kernel only where TMA can stage the input (16-byte row stride); the cp.async
-    // fallback inside it remains for misaligned input pointers.
-    // (8x4 tiles: Wo + 3 <= 4 * 32)
-    return K == 3 && stride == 1 && pad == 1 && W + 3 <= 4 * 32 && (W * 4) % 16 == 0;
+    // 32-pixel (8x4) tiles, whole tile rows per block: at most 32 tiles across
+    // (Wo + 3 <= 4 * 32).  Inputs whose rows TMA cannot stage directly (W % 4 != 0
+    // or a misaligned base) go through a left-padded copy (launch_pipe).
+    return K == 3 && stride == 1 && pad == 1 && W + 3 <= 4 * 32;
 }
 
-void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g) {
+void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
+    // mode 0: TMA on the caller's tensor (xs = 3); 1: TMA on the left-padded copy
+    // (xs = 0); 2: cp.async staging (xs = 0)
     g = PipeGeometry{};
-    g.xs = tma ? 3 : 0;
+    const bool tma = mode != 2;
+    g.xs = mode == 0 ? 3 : 0;
     // 32-pixel thread tiles: 16 FFMA2 per nonzero (scripts/probes/dispatch_probe.cu).
     // 8x4 (tall) keeps the window's 128-bit loads at a 16-byte lane stride (no bank
     // conflicts); 4x8 is the alternative (SPCONV_PIPE_TILE=4x8).
@@ -546,7 +550,8 @@ void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g) {
         }
     }
     g.pitch = best;
-    if (tma && (g.pitch > 256 || g.rs > 256 || (p.W * 4) % 16 != 0)) return;
+    if (tma && (g.pitch > 256 || g.rs > 256)) return;
+    if (mode == 0 && (p.W * 4) % 16 != 0) return;
     g.cc = p.pipe_cc;
     g.nchunks = (p.C + g.cc - 1) / g.cc;
     g.in_words = g.ipb * g.cc * g.rs * g.pitch;
@@ -561,11 +566,55 @@ void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g) {
     g.ok = true;
 }
 
+// Left-padded copy for inputs TMA cannot stage directly (row stride not a
+// multiple of 16 bytes, or a misaligned base): xp[n][c][iy][0] = 0,
+// xp[..][1 + ix] = x[..][ix], zero up to the padded width Wp (multiple of 4).
+__global__ void __launch_bounds__(256) pad_rows_kernel(const float *__restrict__ x, float *__restrict__ xp,
+                                                       int64_t rows, int W, int Wp) {
+    const int q = Wp / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * q;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / q;
+        const int c0 = int(i - row * q) * 4;
+        const float *src = x + row * W;
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ix = c0 + k - 1;
+            v[k] = (ix >= 0 && ix < W) ? __ldg(src + ix) : 0.0f;
+        }
+        reinterpret_cast<float4 *>(xp + row * Wp)[c0 / 4] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
                         cudaStream_t s) {
-    bool use_tma = p.pipe_tma.ok && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && get_encode() != nullptr;
-    const PipeGeometry &g = use_tma ? p.pipe_tma : p.pipe_cp;
+    // staging: 0 = TMA on the caller's tensor (tile columns shifted by 3),
+    //          1 = TMA on a left-padded copy (no shift), 2 = cp.async (fallback)
+    const bool x16 = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    int mode = (p.pipe_tma.ok && x16) ? 0 : p.pipe_pad.ok ? 1 : 2;
+    if (const char *e = std::getenv("SPCONV_PIPE_STAGING")) {
+        if (std::strcmp(e, "cp") == 0) mode = 2;
+        if (std::strcmp(e, "pad") == 0 && p.pipe_pad.ok) mode = 1;
+    }
+    if (mode != 2 && get_encode() == nullptr) mode = 2;
+    const PipeGeometry &g = mode == 0 ? p.pipe_tma : mode == 1 ? p.pipe_pad : p.pipe_cp;
     if (!g.ok) return cudaErrorInvalidConfiguration;
+    const int Wp = ((p.W + 2) + 3) & ~3;
+    float *xp = nullptr;
+    if (mode == 1) {
+        const size_t bytes = size_t(N) * p.C * p.H * Wp * 4;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&xp), bytes, s);
+        if (e != cudaSuccess) return e;
+        const int64_t rows = int64_t(N) * p.C * p.H;
+        const int64_t work = rows * (Wp / 4);
+        const int blocks = int(std::min<int64_t>((work + 255) / 256, 148 * 16));
+        pad_rows_kernel<<<blocks, 256, 0, s>>>(x, xp, rows, p.W, Wp);
+        if ((e = cudaGetLastError()) != cudaSuccess) {
+            cudaFreeAsync(xp, s);
+            return e;
+        }
+    }
     PipeArgs a;
     a.x = x; a.y = y; a.argmax = argmax;
     a.bias = p.d_bias; a.group_rows = p.d_group_rows; a.chunk_start = p.d_chunk_start;
@@ -577,7 +626,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.in_words = g.in_words; a.in_pad = g.in_pad; a.st_bytes = g.st_bytes;
     a.cc = g.cc; a.nchunks = g.nchunks;
     a.gpc = p.gpc; a.num_groups = p.num_groups; a.num_gsets = p.num_gsets;
-    a.tma = use_tma ? 1 : 0;
+    a.tma = mode != 2 ? 1 : 0;
     const int64_t nunits = (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y * p.num_gsets;
     if (nunits > 0x7fffffff) return cudaErrorInvalidConfiguration;
     // persistent: one CTA per SM (the register file holds one 8-warp CTA)
@@ -593,29 +642,43 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
 
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
-    if (use_tma) {
-        cuuint64_t dims[4] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)N};
-        cuuint64_t strides[3] = {(cuuint64_t)p.W * 4, (cuuint64_t)p.H * p.W * 4,
-                                 (cuuint64_t)p.C * p.H * p.W * 4};
+    if (mode != 2) {
+        const cuuint64_t Wt = mode == 0 ? (cuuint64_t)p.W : (cuuint64_t)Wp;
+        cuuint64_t dims[4] = {Wt, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)N};
+        cuuint64_t strides[3] = {Wt * 4, (cuuint64_t)p.H * Wt * 4, (cuuint64_t)p.C * p.H * Wt * 4};
         cuuint32_t box[4] = {(cuuint32_t)g.pitch, (cuuint32_t)g.rs, (cuuint32_t)g.cc, (cuuint32_t)g.ipb};
         cuuint32_t es[4] = {1, 1, 1, 1};
-        CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), dims,
-                                  strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+        CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                  mode == 0 ? const_cast<float *>(x) : xp, dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+        if (r != CUDA_SUCCESS) {
+            if (xp) cudaFreeAsync(xp, s);
+            return cudaErrorInvalidValue;
+        }
     }
     const int grid = int(grid64);
-#define SPC_PIPE_LAUNCH(RR, TT, SS, DD)                                                             \
-    if (p.R == RR && g.T == TT && g.S == SS && p.pipe_dispatch == DD) {                            \
-        if (use_tma) return fused ? launch_one<RR, TT, SS, true, 3, DD>(map, a, grid, g.smem_bytes, s)  \
-                                  : launch_one<RR, TT, SS, false, 3, DD>(map, a, grid, g.smem_bytes, s); \
-        return fused ? launch_one<RR, TT, SS, true, 0, DD>(map, a, grid, g.smem_bytes, s)               \
-                     : launch_one<RR, TT, SS, false, 0, DD>(map, a, grid, g.smem_bytes, s);             \
+    cudaError_t err = cudaErrorInvalidValue;
+#define SPC_PIPE_LAUNCH(RR, TT, SS, DD)                                                                  \
+    if (p.R == RR && g.T == TT && g.S == SS && p.pipe_dispatch == DD) {                                 \
+        if (mode == 0)                                                                                  \
+            err = fused ? launch_one<RR, TT, SS, true, 3, DD, 1>(map, a, grid, g.smem_bytes, s)         \
+                        : launch_one<RR, TT, SS, false, 3, DD, 1>(map, a, grid, g.smem_bytes, s);       \
+        else if (mode == 1)                                                                             \
+            err = fused ? launch_one<RR, TT, SS, true, 0, DD, 1>(map, a, grid, g.smem_bytes, s)         \
+                        : launch_one<RR, TT, SS, false, 0, DD, 1>(map, a, grid, g.smem_bytes, s);       \
+        else                                                                                            \
+            err = fused ? launch_one<RR, TT, SS, true, 0, DD, 0>(map, a, grid, g.smem_bytes, s)         \
+                        : launch_one<RR, TT, SS, false, 0, DD, 0>(map, a, grid, g.smem_bytes, s);       \
     }
     SPC_PIPE_LAUNCH(4, 8, 4, 1)
-    SPC_PIPE_LAUNCH(4, 8, 4, 0)
+    else SPC_PIPE_LAUNCH(4, 8, 4, 0)
 #undef SPC_PIPE_LAUNCH
-    return cudaErrorInvalidValue;
+    if (xp) {
+        cudaError_t e2 = cudaFreeAsync(xp, s);
+        if (err == cudaSuccess) err = e2;
+    }
+    return err;
 }
 
 } // namespace spconv

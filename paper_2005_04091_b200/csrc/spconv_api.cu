@@ -190,12 +190,13 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         // boundaries: each costs a barrier wait, a header load and a refill)
         p->pipe_cc = 1;
         p->max_chunk_bytes = 0;
-        spconv::pipe_geometry(*p, false, p->pipe_cp);
-        spconv::pipe_geometry(*p, true, p->pipe_tma);
-        const int per_ch = std::max(p->pipe_tma.in_words, p->pipe_cp.in_words) * 4;
+        spconv::pipe_geometry(*p, 2, p->pipe_cp);
+        spconv::pipe_geometry(*p, 1, p->pipe_pad);
+        spconv::pipe_geometry(*p, 0, p->pipe_tma);
+        const int per_ch = std::max({p->pipe_tma.in_words, p->pipe_pad.in_words, p->pipe_cp.in_words}) * 4;
         int stage_target = 81920; // measured best on B200
         if (const char *e = std::getenv("SPCONV_PIPE_STAGE_BYTES")) stage_target = std::max(4096, std::atoi(e));
-        const bool tma_feasible = p->pipe_tma.ok;
+        const bool tma_feasible = p->pipe_tma.ok, pad_feasible = p->pipe_pad.ok;
         std::vector<int32_t> cstart;
         // the stream layout depends on cc; shrink cc until the ring fits shared memory
         for (int cc_try = std::max(1, std::min({32, C, stage_target / std::max(per_ch, 1)}));; cc_try /= 2) {
@@ -265,9 +266,12 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
             }
             if (out.size() * 16 > size_t(INT32_MAX)) return SPCONV_ERR_UNSUPPORTED;
             p->max_chunk_bytes = maxb;
-            spconv::pipe_geometry(*p, true, p->pipe_tma);
-            spconv::pipe_geometry(*p, false, p->pipe_cp);
-            if ((p->pipe_cp.ok && (p->pipe_tma.ok || !tma_feasible)) || cc_try == 1) break;
+            spconv::pipe_geometry(*p, 0, p->pipe_tma);
+            spconv::pipe_geometry(*p, 1, p->pipe_pad);
+            spconv::pipe_geometry(*p, 2, p->pipe_cp);
+            if ((p->pipe_cp.ok && (p->pipe_tma.ok || !tma_feasible) && (p->pipe_pad.ok || !pad_feasible)) ||
+                cc_try == 1)
+                break;
         }
         if ((st = upload(&p->d_group_rows, grows.data(), grows.size(), p->device_bytes))) return st;
         if ((st = upload(&p->d_chunk_start, cstart.data(), cstart.size(), p->device_bytes))) return st;
@@ -548,7 +552,9 @@ int spconv_plan_info(spconv_plan_t plan, spconv_plan_info_t *info) {
     info->rows_per_group = p->R;
     info->num_groups = p->num_groups;
     info->device_bytes = p->device_bytes;
-    info->launches_per_call = 1;
+    // the pipelined kernel needs a padding pass first when TMA cannot stage the
+    // caller's rows (W % 4 != 0); a misaligned base pointer adds it at run time
+    info->launches_per_call = (p->kernel == SPCONV_KERNEL_PIPE && !p->pipe_tma.ok) ? 2 : 1;
     return SPCONV_OK;
 }
 

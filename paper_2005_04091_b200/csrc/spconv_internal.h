@@ -86,7 +86,7 @@ struct Plan {
     int pipe_dispatch = 0;         // 0: brx.idx threaded code (default), 1: tap-mask walk
     int32_t *d_chunk_start = nullptr; // [num_gsets * (nchunks + 1)] byte offsets into d_stream2
     uint4 *d_stream2 = nullptr;    // chunks: header (GPC u32 byte offsets) + 16-byte entries
-    PipeGeometry pipe_tma{}, pipe_cp{};
+    PipeGeometry pipe_tma{}, pipe_pad{}, pipe_cp{};
     int64_t device_bytes = 0;
     // spconv_forward_host staging
     std::mutex host_mu;
@@ -103,7 +103,7 @@ cudaError_t launch_generic_fused(const Plan &p, int N, const float *x, float *y,
 
 // kernel_pipe.cu
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad);
-void pipe_geometry(const Plan &p, bool tma, PipeGeometry &g);
+void pipe_geometry(const Plan &p, int mode, PipeGeometry &g); // mode: 0 TMA, 1 TMA on padded copy, 2 cp.async
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                         bool fused, cudaStream_t s);
 

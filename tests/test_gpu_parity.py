@@ -330,3 +330,12 @@ def test_pipe_mask_dispatcher(name, fused, monkeypatch):
     monkeypatch.setenv("SPCONV_PIPE_DISPATCH", "mask")
     _check_full(synthgen.CONFIGS[name], "pipe", fused, N=1 if name == "c5" else 2)
     _check_full(synthgen.CONFIGS[name], "pipe", fused, N=1, integer=True)
+
+
+@pytest.mark.parametrize("staging", ["cp", "pad"])
+@pytest.mark.parametrize("name,fused,N", [("c2", False, 1), ("c3", True, 2), ("c4_80", False, 3)])
+def test_pipe_staging_paths(staging, name, fused, N, monkeypatch):
+    """The pipelined kernel's fallback staging paths (cp.async with zero fill; TMA on a
+    left-padded copy) give the same bits as the oracle."""
+    monkeypatch.setenv("SPCONV_PIPE_STAGING", staging)
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N)
