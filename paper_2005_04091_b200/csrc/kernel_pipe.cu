@@ -604,6 +604,21 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     float *xp = nullptr;
     if (mode == 1) {
         const size_t bytes = size_t(N) * p.C * p.H * Wp * 4;
+        // The workspace comes from the device's default stream-ordered pool; keep
+        // freed blocks cached in it (release threshold = max) so a steady stream of
+        // forwards does not return memory to the driver at every synchronisation.
+        static bool pool_set[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!pool_set[dev & 63]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            cudaGetLastError();
+            pool_set[dev & 63] = true;
+        }
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&xp), bytes, s);
         if (e != cudaSuccess) return e;
         const int64_t rows = int64_t(N) * p.C * p.H;
