@@ -115,6 +115,20 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
  * float[N*F*Ho*Wo].  N == 0 is a no-op.  Asynchronous on `stream`. */
 int spconv_forward(spconv_plan_t plan, int N, const float *x, float *y, void *stream);
 
+/* Epilogue flags of spconv_forward_ex (VGG / ResNet
+ * blocks chain conv layers with fused ReLU and residual add; PAPER.md L503,
+ * L514: operator fusion). */
+enum { SPCONV_EPI_RELU = 1, SPCONV_EPI_RESIDUAL = 2 };
+
+/* y = [ReLU]( (conv(x) + bias) [+ residual] ) elementwise over N*F*Ho*Wo, the
+ * two additions in that order, each one FP32 add (RN); ReLU(v) = v > 0 ? v : +0.
+ * residual: device float[N*F*Ho*Wo], required iff flags has SPCONV_EPI_RESIDUAL;
+ * it may be y itself (in-place accumulate) but must not partially overlap y.
+ * flags == 0 is spconv_forward.  Errors and asynchrony as spconv_forward;
+ * unknown flag bits return SPCONV_ERR_UNSUPPORTED. */
+int spconv_forward_ex(spconv_plan_t plan, int N, const float *x, const float *residual, float *y,
+                      int flags, void *stream);
+
 /* y[N][F][Ho/2][Wo/2] = maxpool2x2(ReLU(conv(x) + bias)); argmax (device
  * int32, same shape, may be NULL) = first-max flat index within each (n,f)
  * conv-output plane.  Requires Ho >= 2 and Wo >= 2 (else SPCONV_ERR_SHAPE).

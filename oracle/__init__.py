@@ -58,6 +58,8 @@ def _load():
         lib.oracle_conv_points_f64.argtypes = shape + [i32p, i32p, f32p, f32p, f32p, L, i64p, f64p]
         lib.oracle_fused_points_f32.argtypes = shape + [i32p, i32p, f32p, f32p, f32p, L, i64p,
                                                          f32p, i32p]
+        lib.oracle_epilogue_f32.argtypes = [f32p, f32p, L, I]
+        lib.oracle_epilogue_f32.restype = None
         _lib = lib
     return _lib
 
@@ -128,6 +130,21 @@ def conv_f32(x, F, K, stride, pad, rowptr, colidx, values, bias=None, nthreads=N
     Ho, Wo = out_dims(H, W, K, stride, pad)
     y = np.empty((N, F, Ho, Wo), np.float32)
     _check(lib.oracle_conv_f32(*args, _p(y, ctypes.c_float), nthreads or default_threads()))
+    return y
+
+
+def conv_ex_f32(x, F, K, stride, pad, rowptr, colidx, values, bias=None, residual=None, relu=False,
+                nthreads=None):
+    """ReLU((conv + bias) + residual) in FP32, the block epilogue of NEXT-3 (R1)."""
+    y = conv_f32(x, F, K, stride, pad, rowptr, colidx, values, bias, nthreads)
+    flags = (1 if relu else 0) | (2 if residual is not None else 0)
+    res = None
+    if residual is not None:
+        res = np.ascontiguousarray(residual, np.float32)
+        if res.shape != y.shape:
+            raise ValueError("residual shape mismatch")
+    _load().oracle_epilogue_f32(_p(y, ctypes.c_float), None if res is None else _p(res, ctypes.c_float),
+                                y.size, flags)
     return y
 
 

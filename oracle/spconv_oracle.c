@@ -308,3 +308,18 @@ int oracle_fused_points_f32(int N, int C, int H, int W, int F, int K, int stride
     }
     return ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* Block epilogue for chained layers (DESIGN.md */
+/* reading R1): y = ReLU((conv + bias) + residual), in that order, one */
+/* FP32 add each; ReLU(v) = v > 0 ? v : +0 (G11).  Applied in place to */
+/* the output of oracle_conv_f32.  flags: bit 0 ReLU, bit 1 residual.  */
+/* ------------------------------------------------------------------ */
+void oracle_epilogue_f32(float *y, const float *residual, int64_t n, int flags) {
+    for (int64_t i = 0; i < n; ++i) {
+        float v = y[i];
+        if (flags & 2) v = v + residual[i];
+        if (flags & 1) v = v > 0.0f ? v : 0.0f;
+        y[i] = v;
+    }
+}

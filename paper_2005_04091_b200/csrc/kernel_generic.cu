@@ -36,8 +36,10 @@ __device__ __forceinline__ float conv_point(const GenericArgs &a, int n, int f, 
     return __fadd_rn(acc, __ldg(a.bias + f));
 }
 
-__global__ void __launch_bounds__(256) generic_conv_kernel(GenericArgs a, int64_t total,
-                                                           float *__restrict__ y) {
+// epi: bit 0 = ReLU, bit 1 = residual add; y = ReLU((acc + bias) + res[i]).
+// res may alias y exactly (each element is read, then written, by one thread).
+__global__ void __launch_bounds__(256) generic_conv_kernel(GenericArgs a, int64_t total, float *y,
+                                                           const float *res, int epi) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int ox = int(i % a.Wo);
@@ -46,7 +48,10 @@ __global__ void __launch_bounds__(256) generic_conv_kernel(GenericArgs a, int64_
         r /= a.Ho;
         const int f = int(r % a.F);
         const int n = int(r / a.F);
-        y[i] = conv_point(a, n, f, oy, ox);
+        float v = conv_point(a, n, f, oy, ox);
+        if (epi & 2) v = __fadd_rn(v, res[i]);
+        if (epi & 1) v = v > 0.0f ? v : 0.0f;
+        y[i] = v;
     }
 }
 
@@ -98,9 +103,10 @@ int grid_for(int64_t total) {
 
 } // namespace
 
-cudaError_t launch_generic_conv(const Plan &p, int N, const float *x, float *y, cudaStream_t s) {
+cudaError_t launch_generic_conv(const Plan &p, int N, const float *x, float *y, cudaStream_t s,
+                                const float *res, int epi) {
     const int64_t total = (int64_t)N * p.F * p.Ho * p.Wo;
-    generic_conv_kernel<<<grid_for(total), 256, 0, s>>>(make_args(p, x), total, y);
+    generic_conv_kernel<<<grid_for(total), 256, 0, s>>>(make_args(p, x), total, y, res, epi);
     return cudaGetLastError();
 }
 

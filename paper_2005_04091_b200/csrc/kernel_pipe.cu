@@ -47,6 +47,7 @@ constexpr int MAX_GPC = 8;
 
 struct PipeArgs {
     const float *x;
+    const float *res; // residual added before the optional ReLU (EPI & 2), may alias y
     float *y;
     int32_t *argmax;
     const float *bias;
@@ -212,7 +213,9 @@ __device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
     return r;
 }
 
-template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG>
+// EPI (conv-only path): bit 0 = ReLU, bit 1 = add a residual tensor; the order is
+// y = ReLU((acc + bias) + residual), two FP32 adds (reading for NEXT-3).
+template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG, int EPI>
 __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -364,23 +367,40 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
             }
         if constexpr (!FUSED) {
             if (!out_ok) continue;
-            float *yp = a.y + ((size_t)n * a.F + f) * a.Ho * a.Wo;
+            const size_t plane = ((size_t)n * a.F + f) * a.Ho * a.Wo;
+            float *yp = a.y + plane;
 #pragma unroll
             for (int t = 0; t < PT; ++t) {
                 const int oy = oy0 + t;
                 if (oy >= a.Ho) continue;
                 float *row = yp + (size_t)oy * a.Wo;
+                const float *rrow = (EPI & 2) ? a.res + plane + (size_t)oy * a.Wo : nullptr;
                 if (XS == 0 && ox0 + PS <= a.Wo && ((reinterpret_cast<uintptr_t>(row + ox0) & 15) == 0) &&
-                    (a.Wo & 3) == 0) {
+                    (a.Wo & 3) == 0 && (!(EPI & 2) || ((reinterpret_cast<uintptr_t>(rrow + ox0) & 15) == 0))) {
 #pragma unroll
-                    for (int q = 0; q < PS; q += 4)
-                        *reinterpret_cast<float4 *>(row + ox0 + q) =
-                            make_float4(v[t][q], v[t][q + 1], v[t][q + 2], v[t][q + 3]);
+                    for (int q = 0; q < PS; q += 4) {
+                        float4 o = make_float4(v[t][q], v[t][q + 1], v[t][q + 2], v[t][q + 3]);
+                        if constexpr ((EPI & 2) != 0) {
+                            const float4 rr = *reinterpret_cast<const float4 *>(rrow + ox0 + q);
+                            o.x = __fadd_rn(o.x, rr.x); o.y = __fadd_rn(o.y, rr.y);
+                            o.z = __fadd_rn(o.z, rr.z); o.w = __fadd_rn(o.w, rr.w);
+                        }
+                        if constexpr ((EPI & 1) != 0) {
+                            o.x = o.x > 0.0f ? o.x : 0.0f; o.y = o.y > 0.0f ? o.y : 0.0f;
+                            o.z = o.z > 0.0f ? o.z : 0.0f; o.w = o.w > 0.0f ? o.w : 0.0f;
+                        }
+                        *reinterpret_cast<float4 *>(row + ox0 + q) = o;
+                    }
                 } else {
 #pragma unroll
                     for (int q = 0; q < PS; ++q) {
                         const int ox = ox0 + q;
-                        if (ox >= 0 && ox < a.Wo) row[ox] = v[t][q];
+                        if (ox >= 0 && ox < a.Wo) {
+                            float o = v[t][q];
+                            if constexpr ((EPI & 2) != 0) o = __fadd_rn(o, rrow[ox]);
+                            if constexpr ((EPI & 1) != 0) o = o > 0.0f ? o : 0.0f;
+                            row[ox] = o;
+                        }
                     }
                 }
             }
@@ -446,9 +466,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG>
+template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG, int EPI = 0>
 cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = pipe_kernel<R, PT, PS, FUSED, XS, DISP, STG>;
+    auto kern = pipe_kernel<R, PT, PS, FUSED, XS, DISP, STG, EPI>;
     static size_t attr_done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -588,7 +608,7 @@ __global__ void __launch_bounds__(256) pad_rows_kernel(const float *__restrict__
 }
 
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
-                        cudaStream_t s) {
+                        cudaStream_t s, const float *res, int epi) {
     // staging: 0 = TMA on the caller's tensor (tile columns shifted by 3),
     //          1 = TMA on a left-padded copy (no shift), 2 = cp.async (fallback)
     const bool x16 = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
@@ -631,7 +651,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         }
     }
     PipeArgs a;
-    a.x = x; a.y = y; a.argmax = argmax;
+    a.x = x; a.y = y; a.argmax = argmax; a.res = res;
     a.bias = p.d_bias; a.group_rows = p.d_group_rows; a.chunk_start = p.d_chunk_start;
     a.stream = reinterpret_cast<const char *>(p.d_stream2);
     a.N = N; a.C = p.C; a.H = p.H; a.W = p.W; a.F = p.F; a.Ho = p.Ho; a.Wo = p.Wo;
@@ -674,21 +694,23 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     }
     const int grid = int(grid64);
     cudaError_t err = cudaErrorInvalidValue;
-#define SPC_PIPE_LAUNCH(RR, TT, SS, DD)                                                                  \
-    if (p.R == RR && g.T == TT && g.S == SS && p.pipe_dispatch == DD) {                                 \
-        if (mode == 0)                                                                                  \
-            err = fused ? launch_one<RR, TT, SS, true, 3, DD, 1>(map, a, grid, g.smem_bytes, s)         \
-                        : launch_one<RR, TT, SS, false, 3, DD, 1>(map, a, grid, g.smem_bytes, s);       \
-        else if (mode == 1)                                                                             \
-            err = fused ? launch_one<RR, TT, SS, true, 0, DD, 1>(map, a, grid, g.smem_bytes, s)         \
-                        : launch_one<RR, TT, SS, false, 0, DD, 1>(map, a, grid, g.smem_bytes, s);       \
-        else                                                                                            \
-            err = fused ? launch_one<RR, TT, SS, true, 0, DD, 0>(map, a, grid, g.smem_bytes, s)         \
-                        : launch_one<RR, TT, SS, false, 0, DD, 0>(map, a, grid, g.smem_bytes, s);       \
+#define SPC_PIPE_MODES(RR, TT, SS, FF, DD, EE)                                                           \
+    err = mode == 0 ? launch_one<RR, TT, SS, FF, 3, DD, 1, EE>(map, a, grid, g.smem_bytes, s)              \
+        : mode == 1 ? launch_one<RR, TT, SS, FF, 0, DD, 1, EE>(map, a, grid, g.smem_bytes, s)              \
+                    : launch_one<RR, TT, SS, FF, 0, DD, 0, EE>(map, a, grid, g.smem_bytes, s);
+    if (p.R == 4 && g.T == 8 && g.S == 4) {
+        if (fused) {
+            if (p.pipe_dispatch == 1) { SPC_PIPE_MODES(4, 8, 4, true, 1, 0) }
+            else { SPC_PIPE_MODES(4, 8, 4, true, 0, 0) }
+        } else if (p.pipe_dispatch == 1) {
+            if (epi != 0) err = cudaErrorNotSupported;
+            else { SPC_PIPE_MODES(4, 8, 4, false, 1, 0) }
+        } else if (epi == 0) { SPC_PIPE_MODES(4, 8, 4, false, 0, 0) }
+        else if (epi == 1) { SPC_PIPE_MODES(4, 8, 4, false, 0, 1) }
+        else if (epi == 2) { SPC_PIPE_MODES(4, 8, 4, false, 0, 2) }
+        else { SPC_PIPE_MODES(4, 8, 4, false, 0, 3) }
     }
-    SPC_PIPE_LAUNCH(4, 8, 4, 1)
-    else SPC_PIPE_LAUNCH(4, 8, 4, 0)
-#undef SPC_PIPE_LAUNCH
+#undef SPC_PIPE_MODES
     if (xp) {
         cudaError_t e2 = cudaFreeAsync(xp, s);
         if (err == cudaSuccess) err = e2;

@@ -434,9 +434,10 @@ int spconv_create(spconv_plan_t *plan, int C, int H, int W, int F, int K, int st
 }
 
 static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax, bool fused,
-               void *stream) {
+               void *stream, const float *res = nullptr, int flags = 0) {
     if (!plan) return SPCONV_ERR_NULLPTR;
     Plan *p = plan;
+    if (flags & ~(SPCONV_EPI_RELU | SPCONV_EPI_RESIDUAL)) return SPCONV_ERR_UNSUPPORTED;
     if (N < 0) return SPCONV_ERR_SHAPE;
     if (fused && (p->Ho < 2 || p->Wo < 2)) return SPCONV_ERR_SHAPE;
     if (N == 0) return SPCONV_OK;
@@ -450,20 +451,28 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     if (overlap(x, xbytes, y, ybytes)) return SPCONV_ERR_ALIAS;
     if (argmax && (overlap(x, xbytes, argmax, ybytes) || overlap(y, ybytes, argmax, ybytes)))
         return SPCONV_ERR_ALIAS;
+    if (flags & SPCONV_EPI_RESIDUAL) {
+        if (!res) return SPCONV_ERR_NULLPTR;
+        if (reinterpret_cast<uintptr_t>(res) & 3) return SPCONV_ERR_ALIGN;
+        // the residual may be y itself (in-place accumulate) but not partially overlap it
+        if (res != y && overlap(res, ybytes, y, ybytes)) return SPCONV_ERR_ALIAS;
+    }
     int st;
     if ((st = check_device_ptr(x, p->device)) || (st = check_device_ptr(y, p->device))) return st;
     if (argmax && (st = check_device_ptr(argmax, p->device))) return st;
+    if ((flags & SPCONV_EPI_RESIDUAL) && (st = check_device_ptr(res, p->device))) return st;
     DeviceGuard guard(p->device);
     if (!guard.ok) return SPCONV_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e;
-    if (p->kernel == SPCONV_KERNEL_PIPE)
-        e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s);
-    else if (p->kernel == SPCONV_KERNEL_TILED)
+    const int epi = fused ? 0 : flags;
+    if (p->kernel == SPCONV_KERNEL_PIPE && !(epi && p->pipe_dispatch == 1))
+        e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s, res, epi);
+    else if (p->kernel == SPCONV_KERNEL_TILED && epi == 0)
         e = spconv::launch_tiled(*p, N, x, y, argmax, fused, s);
-    else
+    else  // the generic kernel serves every epilogue the specialised kernel lacks
         e = fused ? spconv::launch_generic_fused(*p, N, x, y, argmax, s)
-                  : spconv::launch_generic_conv(*p, N, x, y, s);
+                  : spconv::launch_generic_conv(*p, N, x, y, s, res, epi);
     return e == cudaSuccess ? SPCONV_OK : cuda_fail(e);
 }
 
@@ -474,6 +483,11 @@ int spconv_forward(spconv_plan_t plan, int N, const float *x, float *y, void *st
 int spconv_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax,
                               void *stream) {
     return run(plan, N, x, y, argmax, true, stream);
+}
+
+int spconv_forward_ex(spconv_plan_t plan, int N, const float *x, const float *residual, float *y, int flags,
+                      void *stream) {
+    return run(plan, N, x, y, nullptr, false, stream, residual, flags);
 }
 
 int spconv_forward_host(spconv_plan_t plan, int N, const float *x_host, float *y_host, int fused,

@@ -97,7 +97,8 @@ struct Plan {
 };
 
 // kernel_generic.cu
-cudaError_t launch_generic_conv(const Plan &p, int N, const float *x, float *y, cudaStream_t s);
+cudaError_t launch_generic_conv(const Plan &p, int N, const float *x, float *y, cudaStream_t s,
+                                const float *res = nullptr, int epi = 0);
 cudaError_t launch_generic_fused(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                                  cudaStream_t s);
 
@@ -105,7 +106,7 @@ cudaError_t launch_generic_fused(const Plan &p, int N, const float *x, float *y,
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad);
 void pipe_geometry(const Plan &p, int mode, PipeGeometry &g); // mode: 0 TMA, 1 TMA on padded copy, 2 cp.async
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
-                        bool fused, cudaStream_t s);
+                        bool fused, cudaStream_t s, const float *res = nullptr, int epi = 0);
 
 // kernel_tiled.cu
 bool tiled_supported(int C, int H, int W, int F, int K, int stride, int pad);

@@ -25,7 +25,7 @@ KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED
 EXPORTS = ("spconv_create", "spconv_create_ex", "spconv_forward", "spconv_fused_relu_maxpool",
            "spconv_forward_host", "spconv_destroy", "spconv_output_dims", "spconv_plan_info",
            "spconv_status_string", "spconv_abi_version", "spconv_debug_decoded",
-           "spconv_last_cuda_error")
+           "spconv_last_cuda_error", "spconv_forward_ex")
 
 
 class SpconvError(RuntimeError):
@@ -67,6 +67,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.spconv_create_ex.argtypes = lib.spconv_create.argtypes + [ctypes.POINTER(Options)]
     lib.spconv_forward.argtypes = [vp, I, vp, vp, vp]
     lib.spconv_fused_relu_maxpool.argtypes = [vp, I, vp, vp, vp, vp]
+    lib.spconv_forward_ex.argtypes = [vp, I, vp, vp, vp, I, vp]
     lib.spconv_forward_host.argtypes = [vp, I, vp, vp, I, vp]
     lib.spconv_destroy.argtypes = [vp]
     lib.spconv_output_dims.argtypes = [vp, I, I, ctypes.POINTER(ctypes.c_int64)]
@@ -145,6 +146,14 @@ def spconv_create(C, H, W, F, K, stride, pad, rowptr, colidx, values, bias=None,
 
 def spconv_forward(plan, N, x_ptr, y_ptr, stream=None) -> None:
     _check(load_library().spconv_forward(plan, N, x_ptr, y_ptr, _stream_handle(stream)), "spconv_forward")
+
+
+EPI_RELU, EPI_RESIDUAL = 1, 2
+
+
+def spconv_forward_ex(plan, N, x_ptr, residual_ptr, y_ptr, flags, stream=None) -> None:
+    _check(load_library().spconv_forward_ex(plan, N, x_ptr, residual_ptr, y_ptr, flags,
+                                            _stream_handle(stream)), "spconv_forward_ex")
 
 
 def spconv_fused_relu_maxpool(plan, N, x_ptr, y_ptr, argmax_ptr=None, stream=None) -> None:
@@ -231,6 +240,22 @@ class SparseConv2d:
         return out
 
     __call__ = forward
+
+    def forward_ex(self, x, relu=False, residual=None, out=None, stream=None):
+        """y = [ReLU]((conv(x) + bias) [+ residual]) (spconv_forward_ex)."""
+        import torch
+        x = self._check_x(x)
+        N = x.shape[0]
+        if out is None:
+            out = torch.empty(self.output_shape(N), dtype=torch.float32, device=x.device)
+        flags = (EPI_RELU if relu else 0) | (EPI_RESIDUAL if residual is not None else 0)
+        if residual is not None:
+            if tuple(residual.shape) != tuple(out.shape) or residual.dtype != torch.float32 or \
+                    not residual.is_contiguous():
+                raise ValueError("residual must be a contiguous float32 tensor of the output shape")
+        spconv_forward_ex(self.plan, N, x.data_ptr(), None if residual is None else residual.data_ptr(),
+                          out.data_ptr(), flags, stream)
+        return out
 
     def fused_relu_maxpool(self, x, out=None, argmax=None, with_argmax=True, stream=None):
         import torch

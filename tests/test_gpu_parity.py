@@ -339,3 +339,54 @@ def test_pipe_staging_paths(staging, name, fused, N, monkeypatch):
     left-padded copy) give the same bits as the oracle."""
     monkeypatch.setenv("SPCONV_PIPE_STAGING", staging)
     _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N)
+
+
+# ---------------------------------------------------------------- NEXT-3: epilogues and blocks
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("relu,res", [(True, False), (False, True), (True, True)])
+def test_forward_ex_epilogues(kernel, relu, res):
+    cfg = synthgen.CONFIGS["c2"].with_batch(2)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    layer = _layer(cfg, c, b, kernel)
+    x = torch.from_numpy(L.x).cuda()
+    r = synthgen.make_input((2, cfg.F, layer.Ho, layer.Wo), 4242) if res else None
+    rt = torch.from_numpy(r).cuda() if res else None
+    y = layer.forward_ex(x, relu=relu, residual=rt).cpu().numpy()
+    ref = oracle.conv_ex_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, residual=r, relu=relu)
+    assert np.array_equal(bits(y), bits(ref))
+    if res:  # in place: residual == output buffer
+        yt = torch.from_numpy(r).cuda()
+        layer.forward_ex(x, relu=relu, residual=yt, out=yt)
+        assert np.array_equal(bits(yt.cpu().numpy()), bits(ref))
+    layer.close()
+
+
+def test_resnet_and_vgg_blocks_vs_oracle():
+    from paper_2005_04091_b200.blocks import ResNetBasicBlock, VGGBlock, LayerSpec, make_layer
+    N, H, W = 3, 16, 16
+    specs = [LayerSpec(32, 32, 0.203), LayerSpec(32, 32, 0.161)]
+    csrs = [synthgen.make_csr(s.F, s.C, 3, s.density, 900 + 10 * i, 901 + 10 * i) for i, s in enumerate(specs)]
+    biases = [synthgen.make_bias(s.F, 902 + 10 * i) for i, s in enumerate(specs)]
+    x = synthgen.make_input((N, 32, H, W), 950)
+    blk = ResNetBasicBlock(*[make_layer(s, H, W, c, bb) for s, c, bb in zip(specs, csrs, biases)])
+    y = blk(torch.from_numpy(x).cuda()).cpu().numpy()
+    y1 = oracle.conv_ex_f32(x, 32, 3, 1, 1, csrs[0].rowptr, csrs[0].colidx, csrs[0].values, biases[0], relu=True)
+    y2 = oracle.conv_ex_f32(y1, 32, 3, 1, 1, csrs[1].rowptr, csrs[1].colidx, csrs[1].values, biases[1],
+                            residual=x, relu=True)
+    assert np.array_equal(bits(y), bits(y2))
+    blk.close()
+    # VGG-style: 3 layers, last fused with the 2x2 max-pool
+    vspecs = [LayerSpec(16, 32, 0.242), LayerSpec(32, 32, 0.058), LayerSpec(32, 32, 0.01)]
+    vcsrs = [synthgen.make_csr(s.F, s.C, 3, s.density, 960 + 10 * i, 961 + 10 * i) for i, s in enumerate(vspecs)]
+    vb = [synthgen.make_bias(s.F, 962 + 10 * i) for i, s in enumerate(vspecs)]
+    xv = synthgen.make_input((2, 16, 12, 12), 990)
+    vgg = VGGBlock([make_layer(s, 12, 12, c, bb) for s, c, bb in zip(vspecs, vcsrs, vb)])
+    p, am = vgg(torch.from_numpy(xv).cuda(), with_argmax=True)
+    h = xv
+    for s, c, bb in zip(vspecs[:-1], vcsrs[:-1], vb[:-1]):
+        h = oracle.conv_ex_f32(h, s.F, 3, 1, 1, c.rowptr, c.colidx, c.values, bb, relu=True)
+    rp, ra = oracle.fused_f32(h, vspecs[-1].F, 3, 1, 1, vcsrs[-1].rowptr, vcsrs[-1].colidx, vcsrs[-1].values, vb[-1])
+    assert np.array_equal(bits(p.cpu().numpy()), bits(rp)) and np.array_equal(am.cpu().numpy(), ra)
+    vgg.close()

@@ -268,3 +268,43 @@ def test_check_csr_errors():
     ]
     for b in bad:
         assert oracle.check_csr(F, C, K, *b) == -3, b
+
+
+# ---------------------------------------------------------------- NEXT-3 block epilogue (reading R1)
+def test_epilogue_residual_relu_matches_definition():
+    """conv_ex = ReLU((conv + bias) + residual): the composition written out with numpy
+    FP32 adds (IEEE RN, the same single rounding per step) and v > 0 ? v : +0."""
+    cfg = synthgen.CONFIGS["c1"].with_batch(2)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = synthgen.make_bias(cfg.F, 99)
+    res = synthgen.make_input((2, cfg.F, 16, 16), 98)
+    args = (L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+    base = oracle.conv_f32(*args)
+    for relu in (False, True):
+        for r in (None, res):
+            got = oracle.conv_ex_f32(*args, residual=r, relu=relu)
+            want = base.copy() if r is None else (base + r).astype(np.float32)
+            if relu:
+                want = np.where(want > 0, want, np.float32(0.0)).astype(np.float32)
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_resnet_block_chain_vs_torch_float64():
+    """A ResNet basic block composed from oracle layers agrees with the same block in
+    float64 torch (dense conv2d of the densified filters) within the FP32 contract."""
+    torch = pytest.importorskip("torch")
+    C, H, W, N = 8, 9, 7, 2
+    c1 = synthgen.make_csr(C, C, 3, 0.3, 501, 502)
+    c2 = synthgen.make_csr(C, C, 3, 0.2, 503, 504)
+    b1, b2 = synthgen.make_bias(C, 505), synthgen.make_bias(C, 506)
+    x = synthgen.make_input((N, C, H, W), 507)
+    y1 = oracle.conv_ex_f32(x, C, 3, 1, 1, c1.rowptr, c1.colidx, c1.values, b1, relu=True)
+    y2 = oracle.conv_ex_f32(y1, C, 3, 1, 1, c2.rowptr, c2.colidx, c2.values, b2, residual=x, relu=True)
+    w1 = torch.from_numpy(densify(C, C, 3, c1.rowptr, c1.colidx, c1.values)).double()
+    w2 = torch.from_numpy(densify(C, C, 3, c2.rowptr, c2.colidx, c2.values)).double()
+    xt = torch.from_numpy(x).double()
+    t1 = torch.relu(torch.nn.functional.conv2d(xt, w1, torch.from_numpy(b1).double(), padding=1))
+    t2 = torch.relu(torch.nn.functional.conv2d(t1, w2, torch.from_numpy(b2).double(), padding=1) + xt)
+    err = np.abs(y2 - t2.numpy())
+    assert (err <= 1e-4 + 1e-5 * np.abs(t2.numpy())).all(), err.max()
