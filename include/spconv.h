@@ -129,6 +129,23 @@ enum { SPCONV_EPI_RELU = 1, SPCONV_EPI_RESIDUAL = 2 };
 int spconv_forward_ex(spconv_plan_t plan, int N, const float *x, const float *residual, float *y,
                       int flags, void *stream);
 
+/* Bilinear resize ("preceded by an image
+ * resizing step"; the paper does not define it — DESIGN.md reading R2):
+ * half-pixel centres (align_corners = False), source coordinate clamped below at
+ * 0, neighbours clamped to the image, plain FP32 in the order
+ *   s = (o + 0.5) * (in / out) - 0.5;  v = hy*(hx*v00 + lx*v01) + ly*(hx*v10 + lx*v11).
+ * x: device float[N][C][Hin][Win]; y: device float[N][C][Hout][Wout] (not
+ * overlapping x).  Asynchronous on `stream`. */
+int spconv_resize_bilinear(int N, int C, const float *x, int Hin, int Win, float *y, int Hout, int Wout,
+                           void *stream);
+
+/* The Resize-Conv-Relu-Maxpool block: x [N][C][Hin][Win]
+ * is resized to the plan's H x W, then y / argmax as spconv_fused_relu_maxpool.
+ * The resized image is kept in a stream-ordered device workspace between the
+ * two launches (the conv never re-reads x). */
+int spconv_resize_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, int Hin, int Win,
+                                     float *y, int32_t *argmax, void *stream);
+
 /* y[N][F][Ho/2][Wo/2] = maxpool2x2(ReLU(conv(x) + bias)); argmax (device
  * int32, same shape, may be NULL) = first-max flat index within each (n,f)
  * conv-output plane.  Requires Ho >= 2 and Wo >= 2 (else SPCONV_ERR_SHAPE).

@@ -59,6 +59,8 @@ def _load():
         lib.oracle_fused_points_f32.argtypes = shape + [i32p, i32p, f32p, f32p, f32p, L, i64p,
                                                          f32p, i32p]
         lib.oracle_epilogue_f32.argtypes = [f32p, f32p, L, I]
+        lib.oracle_resize_bilinear_f32.argtypes = [I, I, I, I, I, I, f32p, f32p]
+        lib.oracle_resize_bilinear_f32.restype = None
         lib.oracle_epilogue_f32.restype = None
         _lib = lib
     return _lib
@@ -145,6 +147,15 @@ def conv_ex_f32(x, F, K, stride, pad, rowptr, colidx, values, bias=None, residua
             raise ValueError("residual shape mismatch")
     _load().oracle_epilogue_f32(_p(y, ctypes.c_float), None if res is None else _p(res, ctypes.c_float),
                                 y.size, flags)
+    return y
+
+
+def resize_bilinear_f32(x, Hout, Wout):
+    """Bilinear resize, half-pixel centres (reading R2), plain FP32."""
+    x = np.ascontiguousarray(x, np.float32)
+    N, C, Hin, Win = x.shape
+    y = np.empty((N, C, Hout, Wout), np.float32)
+    _load().oracle_resize_bilinear_f32(N, C, Hin, Win, Hout, Wout, _p(x, ctypes.c_float), _p(y, ctypes.c_float))
     return y
 
 

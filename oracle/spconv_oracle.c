@@ -323,3 +323,52 @@ void oracle_epilogue_f32(float *y, const float *residual, int64_t n, int flags) 
         y[i] = v;
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Bilinear resize (SURVEY.md §8(f) NEXT-2 "Resize-Conv-Relu-Maxpool",  */
+/* PAPER.md L503; the paper does not define the resize: DESIGN.md      */
+/* reading R2 = bilinear, half-pixel centres (align_corners = False),  */
+/* source coordinate clamped below at 0, neighbours clamped to the     */
+/* image).  Plain FP32 arithmetic in this exact order, no contraction: */
+/*   s  = (o + 0.5) * (in / out) - 0.5, s = max(s, 0)                  */
+/*   i0 = floor(s), i1 = min(i0 + 1, in - 1), l = s - i0, h = 1 - l    */
+/*   v  = hy * (hx*v00 + lx*v01) + ly * (hx*v10 + lx*v11)              */
+/* ------------------------------------------------------------------ */
+static void resize_coord(int o, int in, int out, int *i0, int *i1, float *l, float *h) {
+    float scale = (float)in / (float)out;
+    float s = ((float)o + 0.5f) * scale - 0.5f;
+    if (s < 0.0f) s = 0.0f;
+    int a = (int)s;
+    if (a > in - 1) a = in - 1;
+    *i0 = a;
+    *i1 = a + 1 < in ? a + 1 : in - 1;
+    *l = s - (float)a;
+    *h = 1.0f - *l;
+}
+
+void oracle_resize_bilinear_f32(int N, int C, int Hin, int Win, int Hout, int Wout, const float *x,
+                                float *y) {
+    for (int64_t nc = 0; nc < (int64_t)N * C; ++nc) {
+        const float *src = x + nc * Hin * Win;
+        float *dst = y + nc * Hout * Wout;
+        for (int oy = 0; oy < Hout; ++oy) {
+            int y0, y1;
+            float ly, hy;
+            resize_coord(oy, Hin, Hout, &y0, &y1, &ly, &hy);
+            for (int ox = 0; ox < Wout; ++ox) {
+                int x0, x1;
+                float lx, hx;
+                resize_coord(ox, Win, Wout, &x0, &x1, &lx, &hx);
+                float t0 = hx * src[y0 * Win + x0];
+                float t1 = lx * src[y0 * Win + x1];
+                float a = t0 + t1;
+                float t2 = hx * src[y1 * Win + x0];
+                float t3 = lx * src[y1 * Win + x1];
+                float b = t2 + t3;
+                float u = hy * a;
+                float w = ly * b;
+                dst[oy * Wout + ox] = u + w;
+            }
+        }
+    }
+}

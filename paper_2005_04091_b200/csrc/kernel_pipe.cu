@@ -607,6 +607,24 @@ __global__ void __launch_bounds__(256) pad_rows_kernel(const float *__restrict__
     }
 }
 
+void keep_pool_cached() {
+    // Workspaces come from the device's default stream-ordered pool; keep freed
+    // blocks cached in it (release threshold = max) so a steady stream of calls
+    // does not return memory to the driver at every synchronisation.
+    static bool pool_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!pool_set[dev & 63]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+        pool_set[dev & 63] = true;
+    }
+}
+
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
                         cudaStream_t s, const float *res, int epi) {
     // staging: 0 = TMA on the caller's tensor (tile columns shifted by 3),
@@ -624,21 +642,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     float *xp = nullptr;
     if (mode == 1) {
         const size_t bytes = size_t(N) * p.C * p.H * Wp * 4;
-        // The workspace comes from the device's default stream-ordered pool; keep
-        // freed blocks cached in it (release threshold = max) so a steady stream of
-        // forwards does not return memory to the driver at every synchronisation.
-        static bool pool_set[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (!pool_set[dev & 63]) {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t thr = ~0ull;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            }
-            cudaGetLastError();
-            pool_set[dev & 63] = true;
-        }
+        keep_pool_cached();
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&xp), bytes, s);
         if (e != cudaSuccess) return e;
         const int64_t rows = int64_t(N) * p.C * p.H;

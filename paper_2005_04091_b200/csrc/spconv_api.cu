@@ -485,6 +485,55 @@ int spconv_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, float *
     return run(plan, N, x, y, argmax, true, stream);
 }
 
+int spconv_resize_bilinear(int N, int C, const float *x, int Hin, int Win, float *y, int Hout, int Wout,
+                           void *stream) {
+    if (N < 0 || C < 1 || Hin < 1 || Win < 1 || Hout < 1 || Wout < 1) return SPCONV_ERR_SHAPE;
+    if (N == 0) return SPCONV_OK;
+    if (!x || !y) return SPCONV_ERR_NULLPTR;
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 3) return SPCONV_ERR_ALIGN;
+    const size_t xb = size_t(N) * C * Hin * Win * 4, yb = size_t(N) * C * Hout * Wout * 4;
+    if (overlap(x, xb, y, yb)) return SPCONV_ERR_ALIAS;
+    cudaPointerAttributes ax, ay;
+    if (cudaPointerGetAttributes(&ax, x) != cudaSuccess || cudaPointerGetAttributes(&ay, y) != cudaSuccess) {
+        cudaGetLastError();
+        return SPCONV_ERR_DEVICE;
+    }
+    if ((ax.type != cudaMemoryTypeDevice && ax.type != cudaMemoryTypeManaged) ||
+        (ay.type != cudaMemoryTypeDevice && ay.type != cudaMemoryTypeManaged) || ax.device != ay.device)
+        return SPCONV_ERR_DEVICE;
+    DeviceGuard guard(ax.device);
+    if (!guard.ok) return SPCONV_ERR_CUDA;
+    cudaError_t e = spconv::launch_resize(x, y, int64_t(N) * C, Hin, Win, Hout, Wout, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SPCONV_OK : cuda_fail(e);
+}
+
+int spconv_resize_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, int Hin, int Win, float *y,
+                                     int32_t *argmax, void *stream) {
+    if (!plan) return SPCONV_ERR_NULLPTR;
+    Plan *p = plan;
+    if (N < 0 || Hin < 1 || Win < 1) return SPCONV_ERR_SHAPE;
+    if (p->Ho < 2 || p->Wo < 2) return SPCONV_ERR_SHAPE;
+    if (N == 0) return SPCONV_OK;
+    if (!x || !y) return SPCONV_ERR_NULLPTR;
+    int st;
+    if ((st = check_device_ptr(x, p->device))) return st;
+    DeviceGuard guard(p->device);
+    if (!guard.ok) return SPCONV_ERR_CUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // the resized image lives in a stream-ordered workspace between the two launches
+    spconv::keep_pool_cached();
+    float *xr = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&xr), size_t(N) * p->C * p->H * p->W * 4, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return SPCONV_ERR_OOM;
+    }
+    st = spconv_resize_bilinear(N, p->C, x, Hin, Win, xr, p->H, p->W, stream);
+    if (st == SPCONV_OK) st = run(plan, N, xr, y, argmax, true, stream);
+    cudaFreeAsync(xr, s);
+    return st;
+}
+
 int spconv_forward_ex(spconv_plan_t plan, int N, const float *x, const float *residual, float *y, int flags,
                       void *stream) {
     return run(plan, N, x, y, nullptr, false, stream, residual, flags);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -101,6 +102,13 @@ cudaError_t launch_generic_conv(const Plan &p, int N, const float *x, float *y, 
                                 const float *res = nullptr, int epi = 0);
 cudaError_t launch_generic_fused(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                                  cudaStream_t s);
+
+// kernel_pipe.cu: keep the default stream-ordered pool's freed blocks cached
+void keep_pool_cached();
+
+// kernel_resize.cu
+cudaError_t launch_resize(const float *x, float *y, int64_t planes, int Hin, int Win, int Hout, int Wout,
+                          cudaStream_t s);
 
 // kernel_pipe.cu
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad);

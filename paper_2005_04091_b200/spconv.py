@@ -25,7 +25,8 @@ KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED
 EXPORTS = ("spconv_create", "spconv_create_ex", "spconv_forward", "spconv_fused_relu_maxpool",
            "spconv_forward_host", "spconv_destroy", "spconv_output_dims", "spconv_plan_info",
            "spconv_status_string", "spconv_abi_version", "spconv_debug_decoded",
-           "spconv_last_cuda_error", "spconv_forward_ex")
+           "spconv_last_cuda_error", "spconv_forward_ex", "spconv_resize_bilinear",
+           "spconv_resize_fused_relu_maxpool")
 
 
 class SpconvError(RuntimeError):
@@ -68,6 +69,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.spconv_forward.argtypes = [vp, I, vp, vp, vp]
     lib.spconv_fused_relu_maxpool.argtypes = [vp, I, vp, vp, vp, vp]
     lib.spconv_forward_ex.argtypes = [vp, I, vp, vp, vp, I, vp]
+    lib.spconv_resize_bilinear.argtypes = [I, I, vp, I, I, vp, I, I, vp]
+    lib.spconv_resize_fused_relu_maxpool.argtypes = [vp, I, vp, I, I, vp, vp, vp]
     lib.spconv_forward_host.argtypes = [vp, I, vp, vp, I, vp]
     lib.spconv_destroy.argtypes = [vp]
     lib.spconv_output_dims.argtypes = [vp, I, I, ctypes.POINTER(ctypes.c_int64)]
@@ -149,6 +152,17 @@ def spconv_forward(plan, N, x_ptr, y_ptr, stream=None) -> None:
 
 
 EPI_RELU, EPI_RESIDUAL = 1, 2
+
+
+def spconv_resize_bilinear(N, C, x_ptr, Hin, Win, y_ptr, Hout, Wout, stream=None) -> None:
+    _check(load_library().spconv_resize_bilinear(N, C, x_ptr, Hin, Win, y_ptr, Hout, Wout,
+                                                 _stream_handle(stream)), "spconv_resize_bilinear")
+
+
+def spconv_resize_fused_relu_maxpool(plan, N, x_ptr, Hin, Win, y_ptr, argmax_ptr=None, stream=None) -> None:
+    _check(load_library().spconv_resize_fused_relu_maxpool(plan, N, x_ptr, Hin, Win, y_ptr, argmax_ptr,
+                                                           _stream_handle(stream)),
+           "spconv_resize_fused_relu_maxpool")
 
 
 def spconv_forward_ex(plan, N, x_ptr, residual_ptr, y_ptr, flags, stream=None) -> None:
@@ -269,6 +283,20 @@ class SparseConv2d:
         spconv_fused_relu_maxpool(self.plan, N, x.data_ptr(), out.data_ptr(),
                                   None if argmax is None else argmax.data_ptr(), stream)
         return out, argmax
+
+    def resize_fused_relu_maxpool(self, x, with_argmax=True, stream=None):
+        """maxpool2x2(ReLU(conv(resize(x)) + bias)), x of any spatial size (NEXT-2)."""
+        import torch
+        if not (x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.dim() == 4 and
+                x.shape[1] == self.C):
+            raise ValueError("x must be a contiguous float32 CUDA tensor [N, C, Hin, Win]")
+        N, _, Hin, Win = x.shape
+        shp = self.output_shape(N, fused=True)
+        out = torch.empty(shp, dtype=torch.float32, device=x.device)
+        am = torch.empty(shp, dtype=torch.int32, device=x.device) if with_argmax else None
+        spconv_resize_fused_relu_maxpool(self.plan, N, x.data_ptr(), Hin, Win, out.data_ptr(),
+                                         None if am is None else am.data_ptr(), stream)
+        return out, am
 
     def forward_host(self, x: np.ndarray, fused=False, with_argmax=True):
         x = np.ascontiguousarray(x, np.float32)

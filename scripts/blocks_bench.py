@@ -71,12 +71,44 @@ def run(name, spec, N, reps, kind):
     blk.close()
 
 
+def run_resize(N, Hin, Win, reps):
+    """Resize-Conv-Relu-Maxpool: the c3 layer (64 -> 64 ch, 56x56,
+    90% sparse) fed by a bilinear resize of an Hin x Win input."""
+    import torch
+    from paper_2005_04091_b200 import SparseConv2d
+    cfg = synthgen.CONFIGS["c3"].with_batch(N)
+    Lr = synthgen.make_layer(cfg, with_input=False)
+    c = Lr.csr
+    layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values,
+                         synthgen.make_bias(cfg.F, 7300))
+    xs = [torch.from_numpy(synthgen.make_input((N, cfg.C, Hin, Win), 7400 + k)).cuda() for k in range(3)]
+    for i in range(3):
+        layer.resize_fused_relu_maxpool(xs[i % 3], with_argmax=False)
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        layer.resize_fused_relu_maxpool(xs[i % 3], with_argmax=False)
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    flops = cfg.useful_flops
+    print(json.dumps({"block": "resize_conv_relu_maxpool", "N": N, "input_hw": [Hin, Win],
+                      "conv_hw": [cfg.H, cfg.W], "density": cfg.density, "ms": round(ms, 4),
+                      "images_per_s": round(N / ms * 1e3, 1), "useful_gflops": round(flops / ms / 1e6, 1),
+                      "launches_per_block": 1 + int(layer.info["launches_per_call"])}), flush=True)
+    layer.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=50)
     a = ap.parse_args()
     run("resnet20_block10", RESNET20_BLOCK10, 256, a.reps, "resnet")
     run("vgg16_block10", VGG16_BLOCK10, 16, a.reps, "vgg")
+    run_resize(32, 112, 112, a.reps)
 
 
 if __name__ == "__main__":

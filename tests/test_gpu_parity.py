@@ -390,3 +390,26 @@ def test_resnet_and_vgg_blocks_vs_oracle():
     rp, ra = oracle.fused_f32(h, vspecs[-1].F, 3, 1, 1, vcsrs[-1].rowptr, vcsrs[-1].colidx, vcsrs[-1].values, vb[-1])
     assert np.array_equal(bits(p.cpu().numpy()), bits(rp)) and np.array_equal(am.cpu().numpy(), ra)
     vgg.close()
+
+
+# ---------------------------------------------------------------- NEXT-2: Resize-Conv-Relu-Maxpool
+@pytest.mark.parametrize("hw_in", [(112, 112), (40, 72), (56, 56)])
+def test_resize_then_fused_block(hw_in):
+    from paper_2005_04091_b200 import spconv as sp
+    cfg = synthgen.CONFIGS["c3"].with_batch(2)
+    L = synthgen.make_layer(cfg, with_input=False)
+    c = L.csr
+    b = _bias(cfg)
+    x = synthgen.make_input((2, cfg.C) + hw_in, 5150 + hw_in[0])
+    xt = torch.from_numpy(x).cuda()
+    # the resize alone, through its own entry point
+    r = torch.empty((2, cfg.C, cfg.H, cfg.W), device="cuda")
+    sp.spconv_resize_bilinear(2, cfg.C, xt.data_ptr(), hw_in[0], hw_in[1], r.data_ptr(), cfg.H, cfg.W)
+    rr = oracle.resize_bilinear_f32(x, cfg.H, cfg.W)
+    assert np.array_equal(bits(r.cpu().numpy()), bits(rr))
+    for kernel in KERNELS:
+        layer = _layer(cfg, c, b, kernel)
+        p, am = layer.resize_fused_relu_maxpool(xt)
+        rp, ra = oracle.fused_f32(rr, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+        assert np.array_equal(bits(p.cpu().numpy()), bits(rp)) and np.array_equal(am.cpu().numpy(), ra)
+        layer.close()

@@ -308,3 +308,23 @@ def test_resnet_block_chain_vs_torch_float64():
     t2 = torch.relu(torch.nn.functional.conv2d(t1, w2, torch.from_numpy(b2).double(), padding=1) + xt)
     err = np.abs(y2 - t2.numpy())
     assert (err <= 1e-4 + 1e-5 * np.abs(t2.numpy())).all(), err.max()
+
+
+# ---------------------------------------------------------------- NEXT-2 resize (reading R2)
+@pytest.mark.parametrize("hw", [(13, 17), (26, 34), (7, 9), (20, 11), (1, 1), (40, 3)])
+def test_resize_bilinear_vs_torch_float64(hw):
+    """Half-pixel bilinear resize == torch interpolate(mode='bilinear', align_corners=False)
+    evaluated in float64, within FP32 rounding of the weights (inputs in [-1, 1))."""
+    x = synthgen.make_input((2, 3, 13, 17), 31337)
+    y = oracle.resize_bilinear_f32(x, *hw)
+    t = torch.nn.functional.interpolate(torch.from_numpy(x).double(), size=hw, mode="bilinear",
+                                        align_corners=False).numpy()
+    assert np.abs(y - t).max() <= 4e-6
+
+
+def test_resize_identity_and_constant():
+    x = synthgen.make_input((1, 2, 9, 11), 4242)
+    assert np.array_equal(oracle.resize_bilinear_f32(x, 9, 11).view(np.uint32), x.view(np.uint32))
+    c = np.full((1, 1, 5, 6), 0.375, np.float32)
+    for hw in [(10, 12), (3, 2), (17, 7)]:
+        assert (oracle.resize_bilinear_f32(c, *hw) == np.float32(0.375)).all()
