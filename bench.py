@@ -392,7 +392,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "pipe", "tiled", "generic"])
     ap.add_argument("--rows", type=int, default=0, help="rows per group R (0 = library default)")
-    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle CPU work")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle CPU work (estimate)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
