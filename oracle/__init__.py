@@ -20,6 +20,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "spconv_oracle.c")
+_SRC_LSTM = os.path.join(_HERE, "lstm_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 # No -ffast-math, no FMA contraction of the plain expressions; fmaf() is the
 # only fused operation (reading G7 in DESIGN.md).
@@ -30,9 +31,10 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (checker only; not the product)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    srcs = [_SRC, _SRC_LSTM]
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(s) for s in srcs):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, *srcs, "-o", tmp, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -61,6 +63,7 @@ def _load():
         lib.oracle_epilogue_f32.argtypes = [f32p, f32p, L, I]
         lib.oracle_resize_bilinear_f32.argtypes = [I, I, I, I, I, I, f32p, f32p]
         lib.oracle_resize_bilinear_f32.restype = None
+        lib.oracle_lstm_f64.argtypes = [I, I, I, I, I, i32p, i64p, i32p, f32p, f32p, f32p, f64p]
         lib.oracle_epilogue_f32.restype = None
         _lib = lib
     return _lib
@@ -209,3 +212,27 @@ def fused_points_f32(x, F, K, stride, pad, rowptr, colidx, values, bias, pts):
     _check(lib.oracle_fused_points_f32(*args, pts.shape[0], _p(pts, ctypes.c_int64),
                                        _p(out, ctypes.c_float), _p(am, ctypes.c_int32)))
     return out, am
+
+
+def lstm_f64(x, layers, H):
+    """Sparse multilayer LSTM (NEXT-4, reading R3), sequential, float64.
+
+    x: float32 [T, B, D]; layers: list of (rowptr[4H+1], colidx, values, bias[4H]) CSR
+    of the fused gate matrix [W | U] (4H x (D_l + H)), gate order i, f, g, o.
+    Returns the last layer's h as float64 [T, B, H]."""
+    x = np.ascontiguousarray(x, np.float32)
+    T, B, D = x.shape
+    L = len(layers)
+    rp = np.concatenate([np.asarray(l[0], np.int32) for l in layers])
+    nnz = [int(len(l[1])) for l in layers]
+    off = np.zeros(L + 1, np.int64)
+    off[1:] = np.cumsum(nnz)
+    ci = np.ascontiguousarray(np.concatenate([np.asarray(l[1], np.int32) for l in layers]))
+    vv = np.ascontiguousarray(np.concatenate([np.asarray(l[2], np.float32) for l in layers]))
+    bb = np.ascontiguousarray(np.concatenate([np.asarray(l[3], np.float32) for l in layers]))
+    h = np.empty((T, B, H), np.float64)
+    st = _load().oracle_lstm_f64(L, D, H, T, B, _p(rp, ctypes.c_int32), _p(off, ctypes.c_int64),
+                                 _p(ci, ctypes.c_int32), _p(vv, ctypes.c_float), _p(bb, ctypes.c_float),
+                                 _p(x, ctypes.c_float), _p(h, ctypes.c_double))
+    _check(st)
+    return h

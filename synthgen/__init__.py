@@ -246,3 +246,29 @@ def make_layer(cfg: LayerConfig, integer: bool = False, with_input: bool = True,
     bias = make_bias(cfg.F, seed_of(k, 3), integer=integer) if cfg.bias else None
     x = make_input((cfg.N, cfg.C, cfg.H, cfg.W), seed_of(k, 2), integer=integer) if with_input else None
     return Layer(cfg, csr, bias, x)
+
+
+# ---------------------------------------------------------------- NEXT-4: sparse multilayer LSTM
+def lstm_seed(layer: int, stream: int) -> int:
+    """Seeds of the LSTM workload: 2005040960 + 10*layer + stream (0 positions,
+    1 values, 3 bias); the input uses stream 2 of layer 0."""
+    return SEED_BASE + 50 + 10 * layer + stream
+
+
+def make_lstm(L: int, D: int, H: int, density: float, T: int, B: int):
+    """Per layer the CSR of the fused gate matrix [W | U] (4H x (D_l + H), gate rows i, f,
+    g, o), bias [4H] and the input x [T, B, D].
+
+    Positions uniform without replacement at ``density`` ("15% as a
+    uniformly distributed density level"); values U[-1, 1) scaled by 1/sqrt(expected
+    nonzeros per row) so the gate pre-activations stay O(1) (input recipe, DESIGN.md);
+    bias U[-0.5, 0.5); inputs U[-1, 1)."""
+    layers = []
+    for l in range(L):
+        Dl = D if l == 0 else H
+        csr = make_csr(4 * H, Dl + H, 1, density, lstm_seed(l, 0), lstm_seed(l, 1))
+        scale = np.float32(1.0 / math.sqrt(max(1.0, density * (Dl + H))))
+        vals = (csr.values * scale).astype(np.float32)
+        layers.append((csr.rowptr, csr.colidx, vals, make_bias(4 * H, lstm_seed(l, 3))))
+    x = make_input((T, B, D), lstm_seed(0, 2))
+    return layers, x

@@ -9,12 +9,16 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "spconv.h")
+HEADERS = sorted(os.path.join(ROOT, "include", h) for h in os.listdir(os.path.join(ROOT, "include"))
+                 if h.endswith(".h"))
 
 
 def _declared():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(spconv_[a-z_]+)\s*\(", src)))
+    names = set()
+    for h in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names |= set(re.findall(r"\b(spconv_[a-z_]+)\s*\(", src))
+    return sorted(names)
 
 
 @pytest.fixture(scope="module")
@@ -35,7 +39,8 @@ def test_library_exports_every_declared_symbol(lib):
     from paper_2005_04091_b200 import spconv
     for name in _declared():
         assert hasattr(lib, name), name
-    assert set(_declared()) == set(spconv.EXPORTS)
+    from paper_2005_04091_b200 import lstm
+    assert set(_declared()) == set(spconv.EXPORTS) | set(lstm.EXPORTS)
 
 
 def test_status_strings_and_version(lib):

@@ -1,0 +1,81 @@
+"""NEXT-4: the sparse multilayer LSTM.
+
+CPU: the oracle (oracle/lstm_oracle.c, reading R3) is pinned to torch.nn.LSTM in
+float64 (a library routine with the same gate equations) and to the zero-weight case.
+GPU (-m gpu): the CUDA wavefront and sequential schedules through the C-ABI agree
+with each other bit for bit (every cell runs the same code on the same inputs, only
+the launch grouping differs) and with the float64 oracle within the FP32 tolerance
+derived in DESIGN.md (R3)."""
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+
+torch = pytest.importorskip("torch")
+
+
+def _torch_lstm(x, layers, D, H):
+    L = len(layers)
+    m = torch.nn.LSTM(D, H, num_layers=L).double()
+    with torch.no_grad():
+        for l, (rp, ci, vv, bb) in enumerate(layers):
+            Dl = D if l == 0 else H
+            G = np.zeros((4 * H, Dl + H))
+            for r in range(4 * H):
+                G[r, ci[rp[r]:rp[r + 1]]] = vv[rp[r]:rp[r + 1]]
+            getattr(m, f"weight_ih_l{l}").copy_(torch.from_numpy(G[:, :Dl]))
+            getattr(m, f"weight_hh_l{l}").copy_(torch.from_numpy(G[:, Dl:]))
+            getattr(m, f"bias_ih_l{l}").copy_(torch.from_numpy(np.asarray(bb, np.float64)))
+            getattr(m, f"bias_hh_l{l}").zero_()
+        out, _ = m(torch.from_numpy(x).double())
+    return out.numpy()
+
+
+@pytest.mark.parametrize("L,D,H,T,B,d", [(1, 5, 4, 1, 1, 0.5), (2, 12, 8, 5, 3, 0.3), (3, 16, 16, 9, 2, 0.15),
+                                         (4, 7, 6, 4, 5, 1.0)])
+def test_oracle_matches_torch_lstm(L, D, H, T, B, d):
+    layers, x = synthgen.make_lstm(L, D, H, d, T, B)
+    h = oracle.lstm_f64(x, layers, H)
+    assert np.abs(h - _torch_lstm(x, layers, D, H)).max() < 1e-12
+
+
+def test_oracle_zero_weights_give_zero():
+    L, D, H, T, B = 2, 6, 4, 3, 2
+    layers = [(np.zeros(4 * H + 1, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float32),
+               np.zeros(4 * H, np.float32)) for _ in range(L)]
+    x = synthgen.make_input((T, B, D), 11)
+    assert (oracle.lstm_f64(x, layers, H) == 0.0).all()
+
+
+def _gpu_case(L, D, H, T, B, d, batch_sample=None):
+    from paper_2005_04091_b200.lstm import SEQUENTIAL, WAVEFRONT, SparseLSTM
+    layers, x = synthgen.make_lstm(L, D, H, d, T, B)
+    net = SparseLSTM(D, H, layers)
+    xt = torch.from_numpy(x).cuda()
+    hw = net(xt, WAVEFRONT).cpu().numpy()
+    hs = net(xt, SEQUENTIAL).cpu().numpy()
+    assert np.array_equal(hw.view(np.uint32), hs.view(np.uint32))
+    cols = np.arange(B) if batch_sample is None else np.asarray(batch_sample)
+    ref = oracle.lstm_f64(np.ascontiguousarray(x[:, cols, :]), layers, H)
+    err = np.abs(hw[:, cols, :] - ref)
+    assert (err <= 2e-5 + 1e-4 * np.abs(ref)).all(), err.max()
+    net.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,D,H,T,B,d", [(1, 5, 4, 1, 1, 0.5), (2, 12, 8, 5, 3, 0.3), (4, 64, 48, 17, 70, 0.15),
+                                         (3, 130, 96, 6, 33, 0.4)])
+def test_gpu_lstm_parity(L, D, H, T, B, d):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _gpu_case(L, D, H, T, B, d)
+
+
+@pytest.mark.gpu
+def test_gpu_lstm_paper_size_sampled():
+    """PAPER.md L510 sizes (4 layers, T=100, H=1024, 15% density), B=64, oracle on a
+    sample of batch columns (they are independent)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _gpu_case(4, 1024, 1024, 100, 64, 0.15, batch_sample=[0, 31, 63])
