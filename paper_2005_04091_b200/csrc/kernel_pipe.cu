@@ -219,7 +219,7 @@ template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG, int EPI>
 __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full_bar[MAXSTAGE];
+    __shared__ __align__(8) uint64_t full_bar[MAXSTAGE], empty_bar[MAXSTAGE];
     __shared__ int done_cnt[MAXSTAGE];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < ns; ++s) {
             mbar_init(smem_u32(&full_bar[s]), STG == 1 ? 1u : 33u);
+            mbar_init(smem_u32(&empty_bar[s]), uint32_t(nwarps));
             done_cnt[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -332,13 +333,19 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
                 }
                 }
             }
-            // release stage s: the last warp to finish with it refills it with stage kk + ns
+            // release stage s: the last warp to finish with it refills it with stage kk + ns.
+            // Every warp arrives on the stage's "empty" mbarrier (release); a shared
+            // counter picks the last arriver, which waits on that barrier phase
+            // (acquire: all warps' reads of the stage happen before) and then orders
+            // the generic-proxy reads before its async-proxy writes (fill_stage).
             __syncwarp();
             int last = 0;
             if (lane == 0) {
+                mbar_arrive(smem_u32(&empty_bar[s]));
                 // monotonic: the n-th use of stage s completes when the count reaches n*nwarps
                 const int old = atomicAdd(&done_cnt[s], 1);
                 last = (old % nwarps) == nwarps - 1;
+                if (last) mbar_wait(smem_u32(&empty_bar[s]), (kk / ns) & 1);
             }
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last && kk + ns < total) {
