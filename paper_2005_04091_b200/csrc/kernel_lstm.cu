@@ -109,6 +109,56 @@ __global__ void __launch_bounds__(256) lstm_cells_kernel(const CellArgs a) {
     }
 }
 
+// Small batches (B < 32): lanes split into NL nonzero slices x BL batch columns
+// (BL = smallest power of two >= B, NL = 32 / BL).  Lane (nl, bl) accumulates the
+// nonzeros j = nl, nl + NL, ... of each gate row for batch column bl; the NL
+// partial sums are then added by a shuffle tree.  (At B = 1 the per-row
+// mapping above would leave 31 lanes idle.)  The summation order differs from the
+// oracle's (tolerance-based parity, reading R3) but is the same for both schedules.
+template <int BL>
+__global__ void __launch_bounds__(256) lstm_cells_small_kernel(const CellArgs a) {
+    constexpr int NL = 32 / BL;
+    const int lane = threadIdx.x & 31;
+    const int bl = lane % BL, nl = lane / BL;
+    const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwork = int64_t(a.ncell) * a.H;
+    if (gw >= nwork) return;
+    const int k = int(gw % a.H);
+    const int ci = int(gw / a.H);
+    const int l = a.l0 + ci, t = a.w - l;
+    const int Dl = l == 0 ? a.D : a.H;
+    const size_t HB = size_t(a.H) * a.B;
+    const float *in = l == 0 ? a.xT + size_t(t) * a.D * a.B
+                             : a.hist + (size_t(l - 1) * (a.T + 1) + (t + 1)) * HB;
+    const float *rec = a.hist + (size_t(l) * (a.T + 1) + t) * HB;
+    const bool okb = bl < a.B;
+    const int32_t *rp = a.rowptr + size_t(l) * (4 * a.H + 1);
+    float gate[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int r = g * a.H + k;
+        const int j0 = __ldg(rp + r), j1 = __ldg(rp + r + 1);
+        float acc = 0.0f;
+        for (int j = j0 + nl; j < j1; j += NL) {
+            const int col = __ldg(a.colidx + j);
+            const float v = __ldg(a.values + j);
+            const float *zr = col < Dl ? in + size_t(col) * a.B : rec + size_t(col - Dl) * a.B;
+            if (okb) acc = __fmaf_rn(v, __ldg(zr + bl), acc);
+        }
+#pragma unroll
+        for (int o = 16; o >= BL; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        gate[g] = __fadd_rn(acc, __ldg(a.bias + size_t(l) * 4 * a.H + r));
+    }
+    if (nl != 0 || !okb) return;
+    float *cp = a.cst + size_t(l) * HB + size_t(k) * a.B;
+    float *hp = a.hist + (size_t(l) * (a.T + 1) + (t + 1)) * HB + size_t(k) * a.B;
+    const float ig = sigm(gate[0]), fg = sigm(gate[1]);
+    const float gg = tanhf(gate[2]), og = sigm(gate[3]);
+    const float c = __fadd_rn(__fmul_rn(fg, cp[bl]), __fmul_rn(ig, gg));
+    cp[bl] = c;
+    hp[bl] = __fmul_rn(og, tanhf(c));
+}
+
 // x[T][B][D] -> xT[T][D][B]
 __global__ void transpose_in_kernel(const float *__restrict__ x, float *__restrict__ xT, int T, int B, int D) {
     const int64_t n = int64_t(T) * B * D;
@@ -317,8 +367,19 @@ int spconv_lstm_forward(spconv_lstm_t plan, int T, int B, const float *x, float 
     a.L = L; a.D = D; a.H = H; a.T = T; a.B = B; a.nbc = (B + 63) / 64;
     auto launch = [&](int w, int l0, int ncell) {
         a.w = w; a.l0 = l0; a.ncell = ncell;
-        const int64_t threads = int64_t(ncell) * H * a.nbc * 32;
-        lstm_cells_kernel<<<int((threads + 255) / 256), 256, 0, s>>>(a);
+        if (B >= 32) {
+            const int64_t threads = int64_t(ncell) * H * a.nbc * 32;
+            lstm_cells_kernel<<<int((threads + 255) / 256), 256, 0, s>>>(a);
+        } else {
+            const int64_t threads = int64_t(ncell) * H * 32;
+            const int blocks = int((threads + 255) / 256);
+            if (B == 1) lstm_cells_small_kernel<1><<<blocks, 256, 0, s>>>(a);
+            else if (B == 2) lstm_cells_small_kernel<2><<<blocks, 256, 0, s>>>(a);
+            else if (B <= 4) lstm_cells_small_kernel<4><<<blocks, 256, 0, s>>>(a);
+            else if (B <= 8) lstm_cells_small_kernel<8><<<blocks, 256, 0, s>>>(a);
+            else if (B <= 16) lstm_cells_small_kernel<16><<<blocks, 256, 0, s>>>(a);
+            else lstm_cells_small_kernel<32><<<blocks, 256, 0, s>>>(a);
+        }
         return cudaGetLastError();
     };
     if (schedule == SPCONV_LSTM_WAVEFRONT) {
