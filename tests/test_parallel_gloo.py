@@ -1,5 +1,6 @@
 """Multi-process host logic of the batch-sharded driver,
-world_size 2 over gloo on CPU: sharding, CSR broadcast, output all-gather.
+world_size 2 over gloo: sharding, CSR broadcast, output all-gather (on CPU with an oracle
+stand-in layer, and -m gpu with two ranks sharing cuda:0 running the CUDA kernels).
 
 The per-rank layer is injected (``layer_factory``); here it is the CPU oracle, so the
 test checks the distribution logic (every image computed exactly once, gathered in
@@ -150,3 +151,59 @@ def test_shard_bounds_partition(n, world):
     assert seen == list(range(n))
     sizes = [shard_bounds(n, world, r)[1] - shard_bounds(n, world, r)[0] for r in range(world)]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _gpu_worker(rank, world, port, n_total, q):
+    """Two ranks sharing cuda:0 (gloo moves the CUDA tensors): CSR broadcast from rank 0
+    as device tensors -> spconv_create from device pointers -> each rank's batch shard
+    through the CUDA kernel -> all-gather.  The NCCL path on a multi-GPU box is the same
+    code with backend "nccl" and one device per rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2005_04091_b200 import SparseConv2d
+        cfg = synthgen.CONFIGS["c2"].with_batch(n_total)
+        L = synthgen.make_layer(cfg)
+        bias = synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3))
+        src = (L.csr.rowptr, L.csr.colidx, L.csr.values, bias) if rank == 0 else (None, None, None, None)
+        dev = torch.device("cuda", 0)
+        layer = ShardedSparseConv2d(cfg.F, *src, device=dev,
+                                    layer_factory=lambda rp, ci, vv, b: SparseConv2d(
+                                        cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, rp, ci, vv, b, device=0))
+        b0, b1 = layer.local_shard(n_total)
+        xs = torch.from_numpy(L.x[b0:b1].copy()).to(dev)
+        y = layer.forward(xs)
+        full = gather_output(y.cpu(), n_total)  # gloo gathers host copies
+        p, am = layer.forward(xs, fused=True)
+        fp = gather_output(p.cpu(), n_total)
+        fa = gather_output(am.cpu(), n_total)
+        if rank == 0:
+            q.put((full.numpy(), fp.numpy(), fa.numpy()))
+        layer.layer.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_ranks_on_one_gpu_match_single_process():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n_total = 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, n_total, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    y, fp, fa = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    cfg = synthgen.CONFIGS["c2"].with_batch(n_total)
+    L = synthgen.make_layer(cfg)
+    bias = synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3))
+    args = (L.x, cfg.F, cfg.K, cfg.stride, cfg.pad, L.csr.rowptr, L.csr.colidx, L.csr.values, bias)
+    assert np.array_equal(y.view(np.uint32), oracle.conv_f32(*args).view(np.uint32))
+    rp, ra = oracle.fused_f32(*args)
+    assert np.array_equal(fp.view(np.uint32), rp.view(np.uint32)) and np.array_equal(fa, ra)
