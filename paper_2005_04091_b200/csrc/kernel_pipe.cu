@@ -33,6 +33,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -59,7 +61,23 @@ struct PipeArgs {
     int cc, nchunks;
     int gpc, num_groups, num_gsets;
     int tma;
+    // ordered stream-K (sk = 1): CTA b owns the contiguous chunk range
+    // [b*U*nch/grid, (b+1)*U*nch/grid) of the U units; a unit cut by a range end is
+    // started by CTA b (its "head", done FIRST, accumulators parked in sk_part slot b)
+    // and finished by CTA b+1 (its "tail", done LAST, continuing from the parked
+    // accumulators), so every output is still one ascending fma chain (FP32 contract).
+    int sk;
+    ulonglong2 *sk_part;              // [grid][gpc][R*PT*PS/4][32 lanes]
+    unsigned long long *sk_flag;      // [grid][gpc]: == epoch when slot (b, warp) is ready
+    unsigned long long epoch;
+    unsigned long long *trace; // debug (SPCONV_PIPE_TRACE): per CTA 8 timestamps, or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -225,6 +243,13 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int ns = a.nstage;
+    unsigned long long *tr = a.trace ? a.trace + size_t(blockIdx.x) * 8 : nullptr;
+    if (tr && threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        tr[0] = gtimer();
+        tr[7] = smid;
+    }
     const uint32_t stage_bytes = uint32_t(a.in_pad + a.st_bytes);
     const uint32_t smem0 = smem_u32(smem);
     // chunk byte offsets of every group set, the group -> output channel table and
@@ -238,8 +263,23 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     // numbered across units so the ring prefetches the next unit's first channels
     // while this unit finishes (and during its epilogue).
     const int nunits = ((a.N + a.ipb - 1) / a.ipb) * a.blocks_y * a.num_gsets;
-    const int my_units = blockIdx.x < nunits ? (nunits - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int total = my_units * a.nchunks;
+    const int nch = a.nchunks;
+    // this CTA's work items, in processing order: [head of unit uh: chunks [0, hA)],
+    // nf whole units, [tail of unit ut: chunks [tc0, nch)]
+    int hA = 0, uh = 0, tc0 = 0, tC = 0, ut = 0, nf, uf0;
+    if (a.sk) {
+        const int64_t tot = int64_t(nunits) * nch;
+        const int64_t s0 = tot * blockIdx.x / gridDim.x, e0 = tot * (blockIdx.x + 1) / gridDim.x;
+        if (e0 % nch) { hA = int(e0 % nch); uh = int(e0 / nch); }
+        if (s0 % nch) { tc0 = int(s0 % nch); tC = nch - tc0; ut = int(s0 / nch); }
+        uf0 = int((s0 + nch - 1) / nch);
+        nf = int(e0 / nch) - uf0;
+    } else {
+        uf0 = blockIdx.x;
+        nf = blockIdx.x < nunits ? (nunits - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    }
+    const int total = hA + nf * nch + tC;
+    auto full_unit = [&](int j) { return a.sk ? uf0 + j : uf0 + j * int(gridDim.x); };
 
     for (int i = threadIdx.x; i < ncs; i += blockDim.x) s_cstart[i] = __ldg(a.chunk_start + i);
     for (int i = threadIdx.x; i < a.num_groups * R; i += blockDim.x) s_rows[i] = __ldg(a.group_rows + i);
@@ -255,8 +295,15 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     __syncthreads();
 
     auto fill = [&](int kk) {
-        const int j = kk / a.nchunks, ch = kk - j * a.nchunks;
-        const Unit un = decode_unit(a, blockIdx.x + j * gridDim.x);
+        int u, ch;
+        if (kk < hA) {
+            u = uh; ch = kk;
+        } else {
+            const int k2 = kk - hA, j = k2 / nch;
+            if (j < nf) { u = full_unit(j); ch = k2 - j * nch; }
+            else { u = ut; ch = tc0 + (k2 - nf * nch); }
+        }
+        const Unit un = decode_unit(a, u);
         const int32_t *cs = s_cstart + un.gs * (a.nchunks + 1);
         const int s = kk % ns;
         fill_stage<XS, STG>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, ch, un.n0, un.ty0 * PT - 1, cs[ch],
@@ -281,21 +328,58 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     const uint32_t ch_bytes = uint32_t(a.rs * a.pitch) * 4u;
 
     constexpr int SH = PS / 2, PAIRS = (PS + 2) / 2;
-    for (int j = 0; j < my_units; ++j) {
-        const Unit un = decode_unit(a, blockIdx.x + j * gridDim.x);
+    static_assert(SH % 2 == 0, "partials are parked as 16-byte pairs");
+    const int nitems = (hA > 0) + nf + (tC > 0);
+    int kk0 = 0;
+    for (int it = 0; it < nitems; ++it) {
+        int u, c0 = 0, kind = 0; // kind: 0 whole unit, 1 head (park), 2 tail (resume)
+        if (hA > 0 && it == 0) {
+            u = uh; kind = 1;
+        } else {
+            const int j = it - (hA > 0);
+            if (j < nf) u = full_unit(j);
+            else { u = ut; c0 = tc0; kind = 2; }
+        }
+        const int c1 = kind == 1 ? hA : nch;
+        const Unit un = decode_unit(a, u);
         const int g = un.gs * a.gpc + warp;
         const bool active = g < a.num_groups; // warp-uniform
 
         uint64_t acc[R][PT][SH];
+        if (kind == 2 && active) {
+            // resume: wait for CTA b-1's parked accumulators of this warp (it parked
+            // them before any other work, so this wait is normally already satisfied)
+            const size_t slot = size_t(blockIdx.x - 1) * a.gpc + warp;
+            if (tr && threadIdx.x == 0) tr[3] = gtimer();
+            unsigned long long f;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a.sk_flag + slot) : "memory");
+            } while (f != a.epoch);
+            const ulonglong2 *src = a.sk_part + slot * (R * PT * SH / 2) * 32 + lane;
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+            for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int t = 0; t < PT; ++t)
+                for (int t = 0; t < PT; ++t)
 #pragma unroll
-                for (int h = 0; h < SH; ++h) acc[r][t][h] = 0ull;
+                    for (int h = 0; h < SH; h += 2) {
+                        const ulonglong2 v2 = __ldcg(src + size_t(((r * PT + t) * SH + h) / 2) * 32);
+                        acc[r][t][h] = v2.x;
+                        acc[r][t][h + 1] = v2.y;
+                    }
+            __syncwarp();
+            if (tr && threadIdx.x == 0) tr[4] = gtimer();
+            if (lane == 0) a.sk_flag[slot] = 0ull; // consumed (graph replays reuse the epoch)
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int t = 0; t < PT; ++t)
+#pragma unroll
+                    for (int h = 0; h < SH; ++h) acc[r][t][h] = 0ull;
+        }
 
-        for (int ch = 0; ch < a.nchunks; ++ch) {
-            const int kk = j * a.nchunks + ch;
+        for (int ch = c0; ch < c1; ++ch) {
+            const int kk = kk0++;
             const int s = kk % ns;
             mbar_wait(smem_u32(&full_bar[s]), (kk / ns) & 1);
             if (active) {
@@ -353,6 +437,24 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
             }
         }
         if (!active) continue;
+        if (kind == 1) {
+            // park: the partial sums go to slot (b, warp) for CTA b+1
+            const size_t slot = size_t(blockIdx.x) * a.gpc + warp;
+            ulonglong2 *dst = a.sk_part + slot * (R * PT * SH / 2) * 32 + lane;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int t = 0; t < PT; ++t)
+#pragma unroll
+                    for (int h = 0; h < SH; h += 2)
+                        __stcg(dst + size_t(((r * PT + t) * SH + h) / 2) * 32, make_ulonglong2(acc[r][t][h], acc[r][t][h + 1]));
+            __threadfence();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.sk_flag + slot), "l"(a.epoch) : "memory");
+            if (tr && threadIdx.x == 0) tr[1] = gtimer();
+            continue;
+        }
 
         // ---------------- epilogue (a6) ----------------
         const int n = un.n0 + im;
@@ -457,6 +559,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         }
     }
     }
+    if (tr && threadIdx.x == 0) tr[2] = gtimer();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -704,6 +807,32 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         }
     }
     const int grid = int(grid64);
+    // ordered stream-K when the units do not divide evenly over the persistent CTAs
+    // and the last partial round is a noticeable share of the work (c2: 256 units on
+    // 148 SMs = 1.73 rounds -> 2 without it)
+    a.sk = 0; a.sk_part = nullptr; a.sk_flag = nullptr; a.epoch = 0;
+    if (nunits > grid && nunits % grid != 0 && nunits < 16 * int64_t(grid)) a.sk = 1;
+    if (const char *e = std::getenv("SPCONV_PIPE_SK")) a.sk = (e[0] == '1' && nunits > grid) ? 1 : 0;
+    void *skw = nullptr;
+    a.trace = nullptr;
+    const bool tracing = std::getenv("SPCONV_PIPE_TRACE") != nullptr;
+    if (tracing && cudaMalloc(&a.trace, size_t(grid) * 64) == cudaSuccess) cudaMemsetAsync(a.trace, 0, size_t(grid) * 64, s);
+    if (a.sk) {
+        static std::atomic<unsigned long long> epochs{0};
+        const int qn = p.R * g.T * g.S / 4;
+        const size_t part_bytes = size_t(grid) * p.gpc * qn * 32 * sizeof(ulonglong2);
+        const size_t flag_bytes = size_t(grid) * p.gpc * sizeof(unsigned long long);
+        keep_pool_cached();
+        cudaError_t e = cudaMallocAsync(&skw, part_bytes + flag_bytes, s);
+        if (e != cudaSuccess) {
+            if (xp) cudaFreeAsync(xp, s);
+            return e;
+        }
+        a.sk_part = reinterpret_cast<ulonglong2 *>(skw);
+        a.sk_flag = reinterpret_cast<unsigned long long *>(static_cast<char *>(skw) + part_bytes);
+        // a tagged, process-unique value: stale workspace contents never equal it
+        a.epoch = 0x5ec0'0000'0000'0000ull | (++epochs & 0x0000'ffff'ffff'ffffull);
+    }
     cudaError_t err = cudaErrorInvalidValue;
 #define SPC_PIPE_MODES(RR, TT, SS, FF, DD, EE)                                                           \
     err = mode == 0 ? launch_one<RR, TT, SS, FF, 3, DD, 1, EE>(map, a, grid, g.smem_bytes, s)              \
@@ -722,6 +851,29 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         else { SPC_PIPE_MODES(4, 8, 4, false, 0, 3) }
     }
 #undef SPC_PIPE_MODES
+    if (a.trace) {
+        // debug dump: one line per CTA (start, head parked, end, tail wait begin/end in ns; SM id)
+        std::vector<unsigned long long> h(size_t(grid) * 8);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[size_t(b) * 8]);
+        if (FILE *f = std::fopen(std::getenv("SPCONV_PIPE_TRACE"), "a")) {
+            for (int b = 0; b < grid; ++b) {
+                const unsigned long long *e = &h[size_t(b) * 8];
+                auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
+                std::fprintf(f, "%d %llu %lld %lld %lld %lld %lld\n", b, e[7], rel(e[0]), rel(e[1]), rel(e[2]),
+                             rel(e[3]), rel(e[4]));
+            }
+            std::fprintf(f, "--\n");
+            std::fclose(f);
+        }
+        cudaFree(a.trace);
+    }
+    if (skw) {
+        cudaError_t e2 = cudaFreeAsync(skw, s);
+        if (err == cudaSuccess) err = e2;
+    }
     if (xp) {
         cudaError_t e2 = cudaFreeAsync(xp, s);
         if (err == cudaSuccess) err = e2;

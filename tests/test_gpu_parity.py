@@ -341,6 +341,24 @@ def test_pipe_staging_paths(staging, name, fused, N, monkeypatch):
     _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N)
 
 
+@pytest.mark.parametrize("sk", ["auto", "1", "0"])
+@pytest.mark.parametrize("name,fused,N", [("c2", False, 19), ("c3", True, 23), ("c4_95", False, 76)])
+def test_pipe_ordered_stream_k(sk, name, fused, N, monkeypatch):
+    """More units than persistent CTAs (c2 N=19: 152 units on 148 SMs): with ordered
+    stream-K a unit cut by a CTA's range is started by one CTA, parked, and finished by
+    the next -- still one ascending fma chain per output, so the bits equal the oracle's
+    with stream-K on, off, and chosen automatically."""
+    if sk != "auto":
+        monkeypatch.setenv("SPCONV_PIPE_SK", sk)
+    _check_full(synthgen.CONFIGS[name], "auto", fused, N=N)
+
+
+def test_pipe_ordered_stream_k_mask_dispatcher(monkeypatch):
+    monkeypatch.setenv("SPCONV_PIPE_SK", "1")
+    monkeypatch.setenv("SPCONV_PIPE_DISPATCH", "mask")
+    _check_full(synthgen.CONFIGS["c2"], "pipe", False, N=19)
+
+
 # ---------------------------------------------------------------- NEXT-3: epilogues and blocks
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("relu,res", [(True, False), (False, True), (True, True)])
