@@ -1,7 +1,8 @@
 """Generate dispatch2_gen.inc: the tap dispatcher of kernel_pipe.cu (v2 kernel).
 
 For one (row group, pipeline stage of input channels) a warp walks a
-shared-memory stream of 16-byte entries {v, v, case, 0}.  Every tap
+shared-memory stream of 16-byte entries {v, v, case of the NEXT entry, 0}
+(the segment starts with a lead entry holding the first case).  Every tap
 case = r*9 + ky*3 + kx selects the FMAs of one CSR nonzero on the thread's
 T x S output tile ("out[n][y][x] +=
 coeff * in[...]"):
@@ -15,11 +16,12 @@ needs the odd pairs (x1,x2),(x3,x4),..., which are not register pairs, and
 issues T*S scalar FFMA.
 
 Dispatch is "threaded code" through one brx.idx jump table, software-
-pipelined one entry deep: the entry of nonzero k+1 is already in registers
-when case k starts, so the jump-table load for k+1 (an indexed constant
-load) is issued at the top of case k and overlaps its FMAs; case k also
-loads entry k+2.  Long case bodies (T*S FMAs) are what hide that latency
-(scripts/probes/dispatch_probe.cu measures it).
+pipelined: the case id of nonzero k+1 is already in a register when case k
+starts, so the jump-table load for k+1 (an indexed constant load) is issued
+at the top of case k and overlaps its FMAs; the tail of case k loads the
+VALUE of entry k+1 straight into the value register (its latency hides under
+the branch) and the case id of entry k+2.  Long case bodies (T*S FMAs) are
+what hide the jump latency (scripts/probes/dispatch_probe.cu measures it).
 
 One walk covers all channels of a pipeline stage: case R*9 ("next channel")
 advances the window pointer by one staged channel and reloads the window
@@ -33,6 +35,9 @@ import sys
 # (R, T, S) variants instantiated by kernel_pipe.cu
 VARIANTS = [(4, 4, 8), (4, 8, 4)]
 MASK_VARIANTS = [(4, 8, 4)]
+# per-case entry load: one 16-byte load (ptxas hoists it and copies the value) or
+# two loads (value, next case) that need no copies but add a shared-memory op
+SPLIT_LOADS = os.environ.get("SPCONV_GEN_SPLIT", "0") == "1"
 
 
 def gen(R: int, T: int, S: int) -> str:
@@ -48,9 +53,21 @@ def gen(R: int, T: int, S: int) -> str:
     def X(i, j):
         return f"%{XBASE + i * PAIRS + j}"
 
+    def head():
+        # case id of entry k+1 (it came with entry k): its jump-table load overlaps
+        # this case's FMAs
+        return ["cvt.u32.u64 %%cn, %%kx;"]
+
     def tail():
-        return ["mov.b64 %%va, %%vb;",
-                "ld.shared.v2.b64 {%%vb, %%kb}, [%%sp];",  # entry k+2
+        # after the FMAs, entry k+1 = {v, v, case of k+2, 0}: the value lands
+        # straight in va (no register rotation copies); sp -> k+2
+        if SPLIT_LOADS:
+            return ["ld.shared.b64 %%va, [%%sp];",
+                    "ld.shared.u32 %%cx, [%%sp+8];",
+                    "cvt.u64.u32 %%kx, %%cx;",
+                    "add.u32 %%sp, %%sp, 16;",
+                    f"brx.idx.uni %%cn, $D{tag}_T;"]
+        return ["ld.shared.v2.b64 {%%va, %%kx}, [%%sp];",
                 "add.u32 %%sp, %%sp, 16;",
                 f"brx.idx.uni %%cn, $D{tag}_T;"]
 
@@ -62,22 +79,23 @@ def gen(R: int, T: int, S: int) -> str:
     tag = f"R{R}T{T}S{S}"
     L = []
     L.append("{")
-    L.append(".reg .b64 %%va, %%vb, %%ka, %%kb;")  # (v,v) and (case,0) of the current / next entry
-    L.append(".reg .b32 %%cn, %%sp, %%v1, %%vd, %%wa;")
+    L.append(".reg .b64 %%va, %%kx;")  # (v, v) of the current entry, (case of the next, 0)
+    L.append(".reg .b32 %%cn, %%cx, %%sp, %%v1, %%vd, %%wa;")
     L.append(".reg .f32 " + ", ".join(f"%%a{i}" for i in range(S)) + ", "
              + ", ".join(f"%%x{i}" for i in range(S + 2)) + ";")
+    # P -> a lead entry whose case field is the first entry's case (the segment's
+    # header entry, or a "next channel" marker when a walk starts mid-stage)
     L.append(f"mov.b32 %%sp, {P};")
-    L.append("ld.shared.v2.b64 {%%va, %%ka}, [%%sp];")
-    L.append("ld.shared.v2.b64 {%%vb, %%kb}, [%%sp+16];")
+    L.append("ld.shared.u32 %%cn, [%%sp+8];")
+    L.append("ld.shared.v2.b64 {%%va, %%kx}, [%%sp+16];")
     L.append("add.u32 %%sp, %%sp, 32;")
-    L.append("cvt.u32.u64 %%cn, %%ka;")
     L.append(f"$D{tag}_T: .branchtargets " + ", ".join(f"$D{tag}_{i}" for i in range(ncase + 2)) + ";")
     L.append(f"brx.idx.uni %%cn, $D{tag}_T;")
     for i in range(ncase):
         # tap-major case numbering: case = (ky*3 + kx)*R + r
         r, ky, kx = i % R, (i // R) // 3, (i // R) % 3
         L.append(f"$D{tag}_{i}:")
-        L.append("cvt.u32.u64 %%cn, %%kb;")  # case of entry k+1 (loaded one case ago)
+        L += head()
         if kx != 1:
             for t in range(T):
                 for h in range(SH):
@@ -97,7 +115,7 @@ def gen(R: int, T: int, S: int) -> str:
         L += tail()
     # next channel: advance the window and reload it (T+2 rows of PAIRS pairs)
     L.append(f"$D{tag}_{ncase}:")
-    L.append("cvt.u32.u64 %%cn, %%kb;")
+    L += head()
     L.append(f"add.u32 {WP}, {WP}, {CHS};")
     L.append(f"mov.b32 %%wa, {WP};")
     for i in range(T + 2):

@@ -59,6 +59,7 @@ struct PipeArgs {
     int N, C, H, W, F, Ho, Wo, Po, Qo;
     int xs, tiles_x, tiles_y, ipb, tr, lanes, blocks_y, rs, pitch, nstage, in_words, in_pad, st_bytes;
     int cc, nchunks;
+    int band; // 1: the ipb slots of a unit are tile-row bands of the flattened (image, tile row) sequence
     int gpc, num_groups, num_gsets;
     int tma;
     // ordered stream-K (sk = 1): CTA b owns the contiguous chunk range
@@ -144,17 +145,18 @@ __device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(uint3
 // dense value blocks back to back.
 template <int R, int PT, int PS>
 __device__ __forceinline__ void mask_walk(uint64_t (&acc)[R][PT][PS / 2], const unsigned char *wbase,
-                                          const unsigned char *seg, uint32_t seg_s, int ncl, uint32_t row_bytes,
-                                          uint32_t ch_bytes) {
+                                          const unsigned char *seg, uint32_t seg_s, int ncl, int cl0, int cl1,
+                                          uint32_t row_bytes, uint32_t ch_bytes) {
+    // channels [cl0, cl1) of the ncl staged ones (a stream-K head / tail may cover part of a stage)
     constexpr int PAIRS = (PS + 2) / 2;
     const uint64_t *masks = reinterpret_cast<const uint64_t *>(seg);
-    const uint32_t dense0 = uint32_t((ncl * 8 + 15) & ~15); // dense value blocks start 16-byte aligned
+    const uint32_t dense0 = uint32_t((ncl * 8 + 15) & ~15) + uint32_t(cl0) * 9u * R * 8u; // 16-byte aligned blocks
     uint32_t vb = seg_s + dense0;
     uint64_t v0[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v0[r] = *reinterpret_cast<const uint64_t *>(seg + dense0 + 8 * r);
 #pragma unroll 1
-    for (int cl = 0; cl < ncl; ++cl) {
+    for (int cl = cl0; cl < cl1; ++cl) {
         uint64_t xw[PT + 2][PAIRS];
         const unsigned char *wptr = wbase + cl * ch_bytes;
 #pragma unroll
@@ -177,6 +179,27 @@ __device__ __forceinline__ void mask_walk(uint64_t (&acc)[R][PT][PS / 2], const 
     }
 }
 
+// Index of the k-th (1-based) entry of a warp's stream segment whose case field
+// is the "next channel" marker (case id `marker`).  Entries are 16-byte {v, v,
+// case of the following entry, 0} behind a lead entry, so that index is the entry
+// BEFORE the marker: setting its case field to "end" ends the walk after channel
+// k-1, and the marker entry (index + 1) is a valid lead entry for a walk starting
+// at channel k.  Warp-cooperative (ballot over 32 entries at a time); the caller
+// asks for k < the stage's channel count, so the marker exists.
+__device__ __forceinline__ int find_marker(const uint4 *seg, int k, int lane, uint32_t marker) {
+    int seen = 0;
+    for (int base = 0;; base += 32) {
+        const unsigned m = __ballot_sync(0xffffffffu, seg[base + lane].z == marker);
+        const int c = __popc(m);
+        if (seen + c >= k) {
+            unsigned mm = m;
+            for (int i = 1; i < k - seen; ++i) mm &= mm - 1;
+            return base + __ffs(mm) - 1;
+        }
+        seen += c;
+    }
+}
+
 // Fill stage s with chunk k (channels [k*cc, k*cc + cc)) of the unit at (n0, iy0)
 // and the unit's stream chunk [c_beg, c_end).  TMA: called by one lane.
 // cp.async: called by a whole warp.
@@ -194,7 +217,19 @@ __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeAr
         // TMA: XS == 3 loads the caller's tensor from ix = -4 (16-byte aligned start);
         // XS == 0 loads the left-padded copy (column 0 = the zero pad) from column 0
         mbar_expect_tx(fb, uint32_t(a.in_words) * 4u + st_bytes);
-        tma_load_4d(tmap, fb, dst_in, XS == 3 ? -4 : 0, iy0, k * a.cc, n0);
+        if (a.band) {
+            // one box per band: [cc][PT + 2][pitch] of image n from row ty*PT - 1
+            const int nb = a.N * a.tiles_y;
+            const uint32_t slot_bytes = uint32_t(a.cc * a.rs * a.pitch) * 4u;
+            for (int b = 0; b < a.ipb; ++b) {
+                const int v = min(n0 + b, nb - 1); // a ragged last unit reloads the last band (not stored)
+                const int n = v / a.tiles_y, ty = v - n * a.tiles_y;
+                tma_load_4d(tmap, fb, dst_in + uint32_t(b) * slot_bytes, XS == 3 ? -4 : 0, ty * (a.rs - 2) - 1,
+                            k * a.cc, n);
+            }
+        } else {
+            tma_load_4d(tmap, fb, dst_in, XS == 3 ? -4 : 0, iy0, k * a.cc, n0);
+        }
         bulk_load(dst_st, a.stream + c_beg, st_bytes, fb);
     } else {
         if (lane == 0) {
@@ -209,7 +244,13 @@ __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeAr
             const int cl = rem / per_ch;
             rem -= cl * per_ch;
             const int r = rem / a.pitch, col = rem - r * a.pitch;
-            const int n = n0 + im, c = k * a.cc + cl, iy = iy0 + r, ix = col - (XS + 1);
+            int n = n0 + im, iyb = iy0;
+            if (a.band) {
+                const int v = n0 + im;
+                n = v / a.tiles_y;
+                iyb = (v - n * a.tiles_y) * (a.rs - 2) - 1;
+            }
+            const int c = k * a.cc + cl, iy = iyb + r, ix = col - (XS + 1);
             const bool ok = n < a.N && c < a.C && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
             const float *src = ok ? a.x + (((size_t)n * a.C + c) * a.H + iy) * a.W + ix : a.x;
             cp_async_4(dst_in + uint32_t(e) * 4u, src, ok);
@@ -226,6 +267,11 @@ __device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
     Unit r;
     r.gs = u % a.num_gsets;
     u /= a.num_gsets;
+    if (a.band) { // n0 = first band of the unit
+        r.ty0 = 0;
+        r.n0 = u * a.ipb;
+        return r;
+    }
     r.ty0 = (u % a.blocks_y) * a.tr;
     r.n0 = (u / a.blocks_y) * a.ipb;
     return r;
@@ -262,23 +308,41 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     // persistent CTA: units blockIdx.x, blockIdx.x + gridDim.x, ...; stages are
     // numbered across units so the ring prefetches the next unit's first channels
     // while this unit finishes (and during its epilogue).
-    const int nunits = ((a.N + a.ipb - 1) / a.ipb) * a.blocks_y * a.num_gsets;
+    const int nunits = (a.band ? (a.N * a.tiles_y + a.ipb - 1) / a.ipb : ((a.N + a.ipb - 1) / a.ipb) * a.blocks_y) *
+                       a.num_gsets;
     const int nch = a.nchunks;
-    // this CTA's work items, in processing order: [head of unit uh: chunks [0, hA)],
-    // nf whole units, [tail of unit ut: chunks [tc0, nch)]
-    int hA = 0, uh = 0, tc0 = 0, tC = 0, ut = 0, nf, uf0;
-    if (a.sk) {
-        const int64_t tot = int64_t(nunits) * nch;
-        const int64_t s0 = tot * blockIdx.x / gridDim.x, e0 = tot * (blockIdx.x + 1) / gridDim.x;
-        if (e0 % nch) { hA = int(e0 % nch); uh = int(e0 / nch); }
-        if (s0 % nch) { tc0 = int(s0 % nch); tC = nch - tc0; ut = int(s0 / nch); }
-        uf0 = int((s0 + nch - 1) / nch);
-        nf = int(e0 / nch) - uf0;
-    } else {
-        uf0 = blockIdx.x;
-        nf = blockIdx.x < nunits ? (nunits - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    // this CTA's work items, in processing order: [head of unit uh: channels [0, hc),
+    // chunks [0, hA)], nf whole units, [tail of unit ut: channels [tcs, C), chunks
+    // [tc0, nch)].  Stream-K ranges are counted in input channels, so a split can fall
+    // inside a stage: the head walks only the first channels of its last stage, the
+    // tail starts its first stage part-way (find_marker).
+    // The schedule lives in shared memory and is re-read where needed: values kept
+    // in registers across the dispatcher's asm would cost it registers (measured: one
+    // extra MOV on every case's jump-target path, -4% on c5).
+    struct Sched {
+        int hA, uh, tc0, tC, ut, nf, uf0, hc, tcs, total;
+    };
+    __shared__ Sched sch;
+    if (threadIdx.x == 0) {
+        Sched q{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (a.sk) {
+            const int C = a.C;
+            const int64_t tot = int64_t(nunits) * C;
+            const int64_t s0 = tot * blockIdx.x / gridDim.x, e0 = tot * (blockIdx.x + 1) / gridDim.x;
+            if (e0 % C) { q.hc = int(e0 % C); q.uh = int(e0 / C); q.hA = (q.hc + a.cc - 1) / a.cc; }
+            if (s0 % C) { q.tcs = int(s0 % C); q.ut = int(s0 / C); q.tc0 = q.tcs / a.cc; q.tC = nch - q.tc0; }
+            q.uf0 = int((s0 + C - 1) / C);
+            q.nf = int(e0 / C) - q.uf0;
+        } else {
+            q.uf0 = blockIdx.x;
+            q.nf = int(blockIdx.x) < nunits ? (nunits - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+        }
+        q.total = q.hA + q.nf * nch + q.tC;
+        sch = q;
     }
-    const int total = hA + nf * nch + tC;
+    __syncthreads();
+    const int &hA = sch.hA, &uh = sch.uh, &tc0 = sch.tc0, &tC = sch.tC, &ut = sch.ut, &nf = sch.nf,
+              &uf0 = sch.uf0, &hc = sch.hc, &tcs = sch.tcs, &total = sch.total;
     auto full_unit = [&](int j) { return a.sk ? uf0 + j : uf0 + j * int(gridDim.x); };
 
     for (int i = threadIdx.x; i < ncs; i += blockDim.x) s_cstart[i] = __ldg(a.chunk_start + i);
@@ -294,7 +358,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     }
     __syncthreads();
 
-    auto fill = [&](int kk) {
+    auto fill = [&](int kk, int s) {
         int u, ch;
         if (kk < hA) {
             u = uh; ch = kk;
@@ -305,14 +369,13 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         }
         const Unit un = decode_unit(a, u);
         const int32_t *cs = s_cstart + un.gs * (a.nchunks + 1);
-        const int s = kk % ns;
         fill_stage<XS, STG>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, ch, un.n0, un.ty0 * PT - 1, cs[ch],
                        cs[ch + 1], lane);
     };
     if (warp == 0) {
         for (int kk = 0; kk < min(ns, total); ++kk) {
             if (STG == 1 && lane != 0) continue;
-            fill(kk);
+            fill(kk, kk);
         }
     }
 
@@ -330,7 +393,9 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
     constexpr int SH = PS / 2, PAIRS = (PS + 2) / 2;
     static_assert(SH % 2 == 0, "partials are parked as 16-byte pairs");
     const int nitems = (hA > 0) + nf + (tC > 0);
-    int kk0 = 0;
+    // ring position, kept incrementally (no integer division per stage):
+    // kk = chunk sequence number, s = kk % ns, rnd = kk / ns
+    int kk = 0, s = 0, rnd = 0;
     for (int it = 0; it < nitems; ++it) {
         int u, c0 = 0, kind = 0; // kind: 0 whole unit, 1 head (park), 2 tail (resume)
         if (hA > 0 && it == 0) {
@@ -379,22 +444,41 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         }
 
         for (int ch = c0; ch < c1; ++ch) {
-            const int kk = kk0++;
-            const int s = kk % ns;
-            mbar_wait(smem_u32(&full_bar[s]), (kk / ns) & 1);
+            mbar_wait(smem_u32(&full_bar[s]), rnd & 1);
             if (active) {
                 const unsigned char *stage = smem + size_t(s) * stage_bytes;
                 const uint32_t st_base = smem0 + uint32_t(s) * stage_bytes + uint32_t(a.in_pad);
                 const uint32_t seg_off = reinterpret_cast<const uint32_t *>(stage + a.in_pad)[warp];
+                // channels [cl0, cl1) of this stage: all of them except at a stream-K split
+                const int ncl = min(a.cc, a.C - ch * a.cc);
+                int cl0 = 0, cl1 = ncl;
+                if (kind == 1 && ch == c1 - 1) cl1 = hc - ch * a.cc;
+                if (kind == 2 && ch == c0) cl0 = tcs - ch * a.cc;
                 if constexpr (DISP == 1) {
-                    const int ncl = min(a.cc, a.C - ch * a.cc);
                     mask_walk<R, PT, PS>(acc, stage + win_off, stage + a.in_pad + seg_off, st_base + seg_off, ncl,
-                                         row_bytes, ch_bytes);
+                                         cl0, cl1, row_bytes, ch_bytes);
                 } else {
                 uint32_t sp = st_base + seg_off;
                 uint32_t wp = smem0 + uint32_t(s) * stage_bytes + win_off; // first channel's window
                 uint64_t xw[PT + 2][PAIRS];
                 const unsigned char *wptr = stage + win_off;
+                if (cl0 > 0 || cl1 < ncl) { // warp-uniform, at most twice per CTA
+                    uint4 *seg = reinterpret_cast<uint4 *>(smem + size_t(s) * stage_bytes + a.in_pad + seg_off);
+                    if (cl1 < ncl) {
+                        // end the walk after channel cl1 - 1: its marker becomes "end" (this
+                        // warp's private copy of the segment; the refill overwrites it)
+                        const int j = find_marker(seg, cl1, lane, 9u * R);
+                        if (lane == 0) seg[j].z = 9u * R + 1u;
+                        __syncwarp();
+                    }
+                    if (cl0 > 0) {
+                        // start at channel cl0: the marker entry before it is the lead entry
+                        const int j = find_marker(seg, cl0, lane, 9u * R);
+                        sp += uint32_t(j + 1) * 16u;
+                        wp += uint32_t(cl0) * ch_bytes;
+                        wptr += size_t(cl0) * ch_bytes;
+                    }
+                }
 #pragma unroll
                 for (int i = 0; i < PT + 2; ++i) {
 #pragma unroll
@@ -428,12 +512,17 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
                 mbar_arrive(smem_u32(&empty_bar[s]));
                 // monotonic: the n-th use of stage s completes when the count reaches n*nwarps
                 const int old = atomicAdd(&done_cnt[s], 1);
-                last = (old % nwarps) == nwarps - 1;
-                if (last) mbar_wait(smem_u32(&empty_bar[s]), (kk / ns) & 1);
+                last = old == rnd * nwarps + nwarps - 1;
+                if (last) mbar_wait(smem_u32(&empty_bar[s]), rnd & 1);
             }
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last && kk + ns < total) {
-                if (STG == 0 || lane == 0) fill(kk + ns);
+                if (STG == 0 || lane == 0) fill(kk + ns, s); // (kk + ns) % ns == s
+            }
+            ++kk;
+            if (++s == ns) {
+                s = 0;
+                ++rnd;
             }
         }
         if (!active) continue;
@@ -457,8 +546,12 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         }
 
         // ---------------- epilogue (a6) ----------------
-        const int n = un.n0 + im;
-        const int ty = un.ty0 + tyl;
+        int n = un.n0 + im, ty = un.ty0 + tyl;
+        if (a.band) {
+            const int v = un.n0 + im;
+            n = v / a.tiles_y;
+            ty = v - n * a.tiles_y;
+        }
         const bool out_ok = lane_ok && n < a.N && ty < a.tiles_y;
         const int oy0 = ty * PT, ox0 = tx * PS - XS;
 #pragma unroll
@@ -666,8 +759,21 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
         g.ipb = 1;
         g.tr = std::min(g.tiles_y, 32 / g.tiles_x);
     }
+    // band mode: when whole-image blocks of tr tile rows leave a ragged last block
+    // (c2: 7 tile rows in blocks of 2), a unit takes tr bands of ONE tile row each
+    // from the flattened (image, tile row) sequence instead, each staged with its
+    // own halo -- no half-empty units (SPCONV_PIPE_BANDS=0 disables)
+    g.band = 0;
+    if (g.ipb == 1 && g.tr > 1 && g.tiles_y % g.tr != 0) {
+        const char *e = std::getenv("SPCONV_PIPE_BANDS");
+        if (!(e && e[0] == '0')) {
+            g.band = 1;
+            g.ipb = g.tr;
+            g.tr = 1;
+        }
+    }
     g.lanes = g.ipb * g.tr * g.tiles_x;
-    g.blocks_y = (g.tiles_y + g.tr - 1) / g.tr;
+    g.blocks_y = g.band ? 1 : (g.tiles_y + g.tr - 1) / g.tr;
     g.rs = PT * g.tr + 2;
     // smem columns read: window of the last tile ends at 4*(tiles_x-1) + 5
     const int need = ((PS * g.tiles_x + 2) + 3) & ~3;
@@ -773,10 +879,12 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.xs = g.xs; a.tiles_x = g.tiles_x; a.tiles_y = g.tiles_y; a.ipb = g.ipb; a.tr = g.tr;
     a.lanes = g.lanes; a.blocks_y = g.blocks_y; a.rs = g.rs; a.pitch = g.pitch; a.nstage = g.nstage;
     a.in_words = g.in_words; a.in_pad = g.in_pad; a.st_bytes = g.st_bytes;
-    a.cc = g.cc; a.nchunks = g.nchunks;
+    a.cc = g.cc; a.nchunks = g.nchunks; a.band = g.band;
     a.gpc = p.gpc; a.num_groups = p.num_groups; a.num_gsets = p.num_gsets;
     a.tma = mode != 2 ? 1 : 0;
-    const int64_t nunits = (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y * p.num_gsets;
+    const int64_t nblocks = g.band ? (int64_t(N) * g.tiles_y + g.ipb - 1) / g.ipb
+                                   : (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y;
+    const int64_t nunits = nblocks * p.num_gsets;
     if (nunits > 0x7fffffff) return cudaErrorInvalidConfiguration;
     // persistent: one CTA per SM (the register file holds one 8-warp CTA)
     static int sm_count[64] = {};
@@ -795,7 +903,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         const cuuint64_t Wt = mode == 0 ? (cuuint64_t)p.W : (cuuint64_t)Wp;
         cuuint64_t dims[4] = {Wt, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)N};
         cuuint64_t strides[3] = {Wt * 4, (cuuint64_t)p.H * Wt * 4, (cuuint64_t)p.C * p.H * Wt * 4};
-        cuuint32_t box[4] = {(cuuint32_t)g.pitch, (cuuint32_t)g.rs, (cuuint32_t)g.cc, (cuuint32_t)g.ipb};
+        cuuint32_t box[4] = {(cuuint32_t)g.pitch, (cuuint32_t)g.rs, (cuuint32_t)g.cc, (cuuint32_t)(g.band ? 1 : g.ipb)};
         cuuint32_t es[4] = {1, 1, 1, 1};
         CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                                   mode == 0 ? const_cast<float *>(x) : xp, dims, strides, box, es,

@@ -159,9 +159,11 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
     if (p->kernel == SPCONV_KERNEL_PIPE) {
         // Per (group set, pipeline stage of cc channels) chunk: a header of GPC u32
         // byte offsets (one per warp, 16-byte padded) then, per warp, for each channel
-        // of the stage its group's nonzeros as 16-byte entries {v, v, case = r*9 +
-        // ky*3 + kx, 0} ascending by case, followed by a "next channel" marker (case
-        // R*9) or, after the stage's last channel, an "end" marker (R*9+1).
+        // of the stage its group's nonzeros with case = (ky*3 + kx)*R + r, ascending
+        // by case, followed by a "next channel" marker (case R*9) or, after the
+        // stage's last channel, an "end" marker (R*9+1).  Stored as 16-byte entries
+        // {v, v, case of the following entry, 0} behind a lead entry {0, 0, first
+        // case, 0} (gen_dispatch2.py).
         // Ascending case within a channel, channels in order: every output row's
         // taps are consumed in ascending colidx order (the FP32 contract).
         p->gpc = std::min(p->num_groups, 8);
@@ -200,7 +202,15 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         std::vector<int32_t> cstart;
         // the stream layout depends on cc; shrink cc until the ring fits shared memory
         for (int cc_try = std::max(1, std::min({32, C, stage_target / std::max(per_ch, 1)}));; cc_try /= 2) {
-            p->pipe_cc = cc_try;
+            // balanced chunks for the same chunk count (stage boundaries cost ~0.5 us
+            // each on c2): a divisor of C when one gives that count
+            const int nch_try = (C + cc_try - 1) / cc_try;
+            int cc_eq = (C + nch_try - 1) / nch_try; // same chunk count, sizes within one channel
+            for (int d = cc_eq; d <= cc_try; ++d)
+                if (C % d == 0 && C / d == nch_try) { cc_eq = d; break; }
+            if (const char *e = std::getenv("SPCONV_PIPE_CC")) // experiments: force the stage size
+                cc_eq = std::max(1, std::min(cc_try, std::atoi(e)));
+            p->pipe_cc = cc_eq;
             const int cc = p->pipe_cc, nchunks = (C + cc - 1) / cc;
             out.clear();
             const uint32_t NEXT = uint32_t(R * 9), END = uint32_t(R * 9 + 1);
@@ -243,6 +253,10 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                                                          uint32_t(items[i + 1]), uint32_t(items[i + 1] >> 32)));
                             continue;
                         }
+                        // the walk order (case, value) of this warp's stage, then stored with
+                        // each entry carrying the NEXT entry's case behind a lead entry, so the
+                        // dispatcher gets value k+1 and case k+2 with one 16-byte load
+                        std::vector<std::pair<uint32_t, uint32_t>> walk;
                         for (int c = c0; c < c1; ++c) {
                             if (g < p->num_groups) {
                                 auto v = byc[size_t(g)][size_t(c)];
@@ -253,11 +267,15 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                                 for (auto &e : v) {
                                     uint32_t bits;
                                     std::memcpy(&bits, &e.second, 4);
-                                    out.push_back(make_uint4(bits, bits, uint32_t(e.first), 0u));
+                                    walk.push_back({uint32_t(e.first), bits});
                                 }
                             }
-                            out.push_back(make_uint4(0u, 0u, c + 1 < c1 ? NEXT : END, 0u));
+                            walk.push_back({c + 1 < c1 ? NEXT : END, 0u});
                         }
+                        out.push_back(make_uint4(0u, 0u, walk[0].first, 0u));
+                        for (size_t k = 0; k < walk.size(); ++k)
+                            out.push_back(make_uint4(walk[k].second, walk[k].second,
+                                                     k + 1 < walk.size() ? walk[k + 1].first : END, 0u));
                     }
                     std::memcpy(reinterpret_cast<char *>(out.data() + base), offs.data(), offs.size() * 4);
                     maxb = std::max(maxb, int((out.size() - base) * 16));

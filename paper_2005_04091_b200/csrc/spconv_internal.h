@@ -49,7 +49,8 @@ struct PipeGeometry {
     int xs;                  // column shift of the thread tiles (3: TMA, 0: cp.async)
     int T, S;                // thread tile: T output rows x S output columns
     int tiles_x, tiles_y;    // 4x4 thread tiles per image row / column
-    int ipb, tr;             // images per block, tile rows per block (per image)
+    int ipb, tr;             // images (band: tile-row bands) per block, tile rows per block (per image)
+    int band;                // 1: blocks are ipb one-tile-row bands of the flattened (image, tile row) sequence
     int lanes;               // active lanes per consumer warp = ipb * tr * tiles_x
     int blocks_y;            // blocks per image (ipb == 1) along the tile rows
     int rs;                  // staged input rows per image = 4 * tr + 2

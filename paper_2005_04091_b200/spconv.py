@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libspconv.so")
+# SPCONV_LIB: load another build of the same ABI (A/B timing of kernel changes)
+LIB_PATH = os.environ.get("SPCONV_LIB") or os.path.join(_PKG, "libspconv.so")
 
 SPCONV_OK = 0
 STATUS = {0: "OK", -1: "NULLPTR", -2: "SHAPE", -3: "CSR", -4: "UNSUPPORTED", -5: "ALIGN",
