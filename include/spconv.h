@@ -157,7 +157,11 @@ int spconv_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, float *
  * device, runs the forward (fused != 0: the fused block, argmax_host may be
  * NULL), copies the result back and synchronises.  Device staging buffers are
  * owned by the plan and grown on demand (serialised by an internal lock).
- * Host buffers may be pageable or pinned (pinned is faster). */
+ * The batch is split into up to 8 contiguous image chunks (>= 3 MiB of input
+ * each) pipelined over plan-owned streams, so the copy-in of chunk i+1 and
+ * the copy-out of chunk i-1 overlap the forward of chunk i; the result is bitwise
+ * that of one device-side call (images are independent).
+ * Host buffers may be pageable or pinned (pinned is needed for the overlap). */
 int spconv_forward_host(spconv_plan_t plan, int N, const float *x_host, float *y_host,
                         int fused, int32_t *argmax_host);
 

@@ -95,7 +95,12 @@ struct Plan {
     float *d_xbuf = nullptr, *d_ybuf = nullptr;
     int32_t *d_abuf = nullptr;
     size_t xbuf_elems = 0, ybuf_elems = 0;
-    cudaStream_t host_stream = nullptr;
+    cudaStream_t host_stream = nullptr;    // host -> device copies
+    static constexpr int HOST_KSTREAMS = 3;
+    cudaStream_t host_kstream[HOST_KSTREAMS] = {}; // forwards of spconv_forward_host (chunks round-robin)
+    cudaStream_t host_ostream = nullptr;   // device -> host copies
+    static constexpr int MAX_HOST_CHUNKS = 16;
+    cudaEvent_t host_ev_in[MAX_HOST_CHUNKS] = {}, host_ev_k[MAX_HOST_CHUNKS] = {};
 };
 
 // kernel_generic.cu

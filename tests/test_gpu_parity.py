@@ -286,6 +286,35 @@ def test_forward_host_matches():
     assert np.array_equal(bits(p), bits(rp)) and np.array_equal(am, ra)
 
 
+def test_forward_host_chunked_pipeline_matches_device_path():
+    # c2 at N=32 is 25.7 MB of input: spconv_forward_host splits it into 6 chunks on
+    # three streams; every image must come out bitwise as in one device-side call,
+    # and the fused path's argmax too (c3 shape, bias, N=24 -> chunked as well)
+    for name, n, fused in (("c2", 32, False), ("c3", 24, True)):
+        cfg = synthgen.CONFIGS[name].with_batch(n)
+        L = synthgen.make_layer(cfg)
+        c = L.csr
+        b = _bias(cfg) if fused else None
+        layer = _layer(cfg, c, b, "auto")
+        xh = torch.from_numpy(L.x).pin_memory()
+        x = xh.cuda()
+        if fused:
+            p, am = layer.forward_host(xh.numpy(), fused=True)
+            rp, ra = layer.fused_relu_maxpool(x)
+            assert np.array_equal(bits(p), bits(rp.cpu().numpy())) and np.array_equal(am, ra.cpu().numpy())
+            # sampled images against the oracle
+            for i in (0, n - 1):
+                op, oa = oracle.fused_f32(L.x[i:i + 1], cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+                assert np.array_equal(bits(p[i:i + 1]), bits(op)) and np.array_equal(am[i:i + 1], oa)
+        else:
+            y = layer.forward_host(xh.numpy())
+            ry = layer(x)
+            assert np.array_equal(bits(y), bits(ry.cpu().numpy()))
+            for i in (0, 13, n - 1):
+                ref = oracle.conv_f32(L.x[i:i + 1], cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+                assert np.array_equal(bits(y[i:i + 1]), bits(ref))
+
+
 # ---------------------------------------------------------------- GPU self-consistency
 def test_fused_equals_pool_of_forward_and_batch_independence():
     cfg = synthgen.CONFIGS["c3"].with_batch(6)
