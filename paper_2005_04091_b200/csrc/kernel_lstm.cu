@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -36,6 +37,10 @@ struct spconv_lstm_s {
     int32_t *d_colidx = nullptr;
     float *d_values = nullptr;
     float *d_bias = nullptr; // [L][4H]
+    // staged kernel (H % 8 == 0): entries grouped per (layer, chunk, 8-unit block)
+    int32_t *d_off = nullptr; // [L][nzc][4H + 4]
+    int2 *d_ent = nullptr;
+    int nzc = 0, ent_cap = 0;
     int64_t nnz = 0;
 };
 
@@ -106,6 +111,154 @@ __global__ void __launch_bounds__(256) lstm_cells_kernel(const CellArgs a) {
         const float c = __fadd_rn(__fmul_rn(fg, cp[b]), __fmul_rn(ig, gg));
         cp[b] = c;
         hp[b] = __fmul_rn(og, tanhf(c));
+    }
+}
+
+// Batches B >= 32 with B % 4 == 0 (16-byte rows) and H % 8 == 0: the z-staged
+// kernel.  CTA = WPC warps = WPC consecutive hidden units of one cell and a tile of
+// 64 batch columns; warp w owns unit k0 + w (its four gate rows i, f, g, o), lane =
+// batch columns b0 + 2*lane, +1.  Per chunk of ZC rows of the stacked operand
+// z = [input ; h_prev], one cp.async stage (double-buffered) brings into shared
+// memory (i) the ZC x 64 z tile and (ii) the CTA's nonzeros in that chunk, which
+// create() laid out contiguously per (layer, chunk, block of 8 units) as 16-byte
+// aligned groups of {col * ZROW, value} entries with their per-row offsets.  So the
+// walk touches only shared memory: per nonzero one broadcast LDS.64 (entry), one
+// LDS.64 (z), two fma.  Rows' entries stay in ascending column order and chunks
+// ascend, so every gate is the same fma chain as in lstm_cells_kernel (bitwise
+// identical results).
+constexpr int ZC = 64;          // z rows per staged chunk
+constexpr int ZROW = 64 * 4;    // bytes per staged z row (64 batch columns)
+
+struct StagedArgs {
+    CellArgs a;
+    const int2 *ent;    // entries, grouped per (layer, chunk, 8-unit block), groups 16-byte aligned
+    const int32_t *off; // [L][nzc][4H + 4]: entry index of row-local q = kb8*32 + g*8 + w; [4H] = end
+    int nzc;            // chunks per layer = ceil((max(D, H) + H) / ZC)
+    int ent_cap;        // entries per stage buffer (max over CTA blocks and chunks, even)
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// One gate row's entries [j, je) of the staged entry buffer, in order (the row's
+// fma chain), 4 per round so four LDS chains are in flight; no per-entry predicates
+// (ncu: a predicated 4-row interleave was ALU-issue bound at 25 instructions per nonzero).
+__device__ __forceinline__ void walk_row(const int2 *es, int j, int je, const unsigned char *zb, float &a0,
+                                         float &a1) {
+    for (; j + 4 <= je; j += 4) {
+        int2 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) e[u] = es[j + u];
+        float2 z[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) z[u] = *reinterpret_cast<const float2 *>(zb + e[u].x);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float v = __int_as_float(e[u].y);
+            a0 = __fmaf_rn(v, z[u].x, a0);
+            a1 = __fmaf_rn(v, z[u].y, a1);
+        }
+    }
+    for (; j < je; ++j) {
+        const int2 e = es[j];
+        const float2 z = *reinterpret_cast<const float2 *>(zb + e.x);
+        const float v = __int_as_float(e.y);
+        a0 = __fmaf_rn(v, z.x, a0);
+        a1 = __fmaf_rn(v, z.y, a1);
+    }
+}
+
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32) lstm_cells_staged_kernel(const StagedArgs sa) {
+    const CellArgs &a = sa.a;
+    // dynamic smem: [2 stages][ZC * ZROW z bytes | ent_cap * 8 entry bytes | (4*WPC + 4) offsets]
+    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr int NQ = 4 * WPC;                 // gate rows of the CTA
+    const uint32_t ent_bytes = uint32_t(sa.ent_cap) * 8u;
+    const uint32_t stage_bytes = uint32_t(ZC * ZROW) + ent_bytes + uint32_t(NQ + 4) * 4u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nkb = a.H / WPC;
+    const int bt = blockIdx.x % a.nbc;
+    const int kb = (blockIdx.x / a.nbc) % nkb;
+    const int ci = blockIdx.x / (a.nbc * nkb);
+    const int l = a.l0 + ci, t = a.w - l;
+    const int k = kb * WPC + warp;
+    const int Dl = l == 0 ? a.D : a.H, ncol = Dl + a.H;
+    const int nch = (ncol + ZC - 1) / ZC;
+    const size_t HB = size_t(a.H) * a.B;
+    const float *in = l == 0 ? a.xT + size_t(t) * a.D * a.B
+                             : a.hist + (size_t(l - 1) * (a.T + 1) + (t + 1)) * HB;
+    const float *rec = a.hist + (size_t(l) * (a.T + 1) + t) * HB;
+    const int b0 = bt * 64;
+    const uint32_t sm0 = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
+    const int q0 = kb * WPC * 4;                // first row-local index of the CTA (kb8 * 32)
+    const int32_t *offl = sa.off + size_t(l) * sa.nzc * (4 * a.H + 4);
+
+    auto stage = [&](int c, int buf) {
+        const uint32_t base = sm0 + uint32_t(buf) * stage_bytes;
+        for (int e = threadIdx.x; e < ZC * 16; e += WPC * 32) {
+            const int r = e >> 4, q = e & 15;
+            const int col = c * ZC + r, b = b0 + 4 * q;
+            const bool ok = col < ncol && b < a.B;
+            const float *src = ok ? (col < Dl ? in + size_t(col) * a.B : rec + size_t(col - Dl) * a.B) + b : a.xT;
+            cp_async16(base + uint32_t(r * ZROW + q * 16), src, ok);
+        }
+        const int32_t *oc = offl + size_t(c) * (4 * a.H + 4);
+        const int e0 = __ldg(oc + q0), e1 = __ldg(oc + q0 + NQ); // group-aligned: even, 16-byte
+        for (int i = threadIdx.x; 2 * i < e1 - e0; i += WPC * 32)
+            cp_async16(base + uint32_t(ZC * ZROW) + uint32_t(i) * 16u, sa.ent + e0 + 2 * i, true);
+        for (int i = threadIdx.x; i <= NQ; i += WPC * 32)
+            cp_async4(base + uint32_t(ZC * ZROW) + ent_bytes + uint32_t(i) * 4u, oc + q0 + i);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    float acc[4][2] = {};
+    const int w8 = warp >> 3, wl = warp & 7;    // 8-unit block within the CTA, unit within it
+    stage(0, 0);
+    for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) {
+            stage(c + 1, (c + 1) & 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const unsigned char *sb = dsm + size_t(c & 1) * stage_bytes;
+        const int2 *es = reinterpret_cast<const int2 *>(sb + ZC * ZROW);
+        const int32_t *so = reinterpret_cast<const int32_t *>(sb + ZC * ZROW + ent_bytes);
+        // generic pointer such that zb + col * ZROW addresses row col - c * ZC of the tile
+        const unsigned char *zb = sb + lane * 8 - ptrdiff_t(c) * ZC * ZROW;
+        const int eb = so[0];
+        const int qb = w8 * 32 + wl;
+        walk_row(es, so[qb] - eb, so[qb + 1] - eb, zb, acc[0][0], acc[0][1]);
+        walk_row(es, so[qb + 8] - eb, so[qb + 9] - eb, zb, acc[1][0], acc[1][1]);
+        walk_row(es, so[qb + 16] - eb, so[qb + 17] - eb, zb, acc[2][0], acc[2][1]);
+        walk_row(es, so[qb + 24] - eb, so[qb + 25] - eb, zb, acc[3][0], acc[3][1]);
+        __syncthreads(); // buffer c & 1 is refilled by the next iteration's stage()
+    }
+    float gate[4][2];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const float bb = __ldg(a.bias + size_t(l) * 4 * a.H + g * a.H + k);
+        gate[g][0] = __fadd_rn(acc[g][0], bb);
+        gate[g][1] = __fadd_rn(acc[g][1], bb);
+    }
+    float *cp = a.cst + size_t(l) * HB + size_t(k) * a.B;
+    float *hp = a.hist + (size_t(l) * (a.T + 1) + (t + 1)) * HB + size_t(k) * a.B;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int b = b0 + 2 * lane + e;
+        if (b >= a.B) continue;
+        const float ig = sigm(gate[0][e]), fg = sigm(gate[1][e]);
+        const float gg = tanhf(gate[2][e]), og = sigm(gate[3][e]);
+        const float cc = __fadd_rn(__fmul_rn(fg, cp[b]), __fmul_rn(ig, gg));
+        cp[b] = cc;
+        hp[b] = __fmul_rn(og, tanhf(cc));
     }
 }
 
@@ -214,6 +367,8 @@ void free_lstm(spconv_lstm_s *p) {
     cudaFree(p->d_colidx);
     cudaFree(p->d_values);
     cudaFree(p->d_bias);
+    cudaFree(p->d_off);
+    cudaFree(p->d_ent);
     if (prev >= 0) cudaSetDevice(prev);
     delete p;
 }
@@ -290,9 +445,55 @@ int spconv_lstm_create(spconv_lstm_t *plan, int L, int D, int H, const int32_t *
     }
     for (float b : bb)
         if (!std::isfinite(b)) return SPCONV_ERR_CSR;
+    // staged-kernel layout (H % 8 == 0): for each layer l and chunk c of ZC z rows,
+    // for each block of 8 hidden units, the 32 gate rows (q = g*8 + w, row = g*H +
+    // 8*kb8 + w) each contribute their nonzeros with column in the chunk, as entries
+    // {col * ZROW, value bits}; every block's group is padded to an even count so it
+    // starts 16-byte aligned.  off[l][c][kb8*32 + q] = entry index of the row's first.
+    const int nzc = (std::max(D, H) + H + ZC - 1) / ZC;
+    std::vector<int32_t> offs;
+    std::vector<int2> ent;
+    int ent_cap = 0;
+    if (H % 8 == 0) {
+        const size_t stride = size_t(4) * H + 4;
+        offs.assign(size_t(L) * nzc * stride, 0);
+        ent.reserve(static_cast<size_t>(nnz + int64_t(L) * nzc * (H / 8)));
+        std::vector<int32_t> cur(size_t(4) * H);
+        for (int l = 0; l < L; ++l) {
+            const int32_t *r = rp.data() + size_t(l) * (4 * H + 1);
+            for (int row = 0; row < 4 * H; ++row) cur[size_t(row)] = r[row];
+            for (int c = 0; c < nzc; ++c) {
+                int32_t *o = offs.data() + (size_t(l) * nzc + c) * stride;
+                for (int kb8 = 0; kb8 < H / 8; ++kb8) {
+                    for (int q = 0; q < 32; ++q) {
+                        const int row = (q / 8) * H + kb8 * 8 + q % 8;
+                        o[kb8 * 32 + q] = int32_t(ent.size());
+                        int32_t &j = cur[size_t(row)];
+                        for (; j < r[row + 1] && ci[size_t(j)] < (c + 1) * ZC; ++j) {
+                            int vb;
+                            std::memcpy(&vb, &vv[size_t(j)], 4);
+                            ent.push_back(make_int2(ci[size_t(j)] * ZROW, vb));
+                        }
+                    }
+                    // pad to 16 bytes with a zero-valued entry on a column of this chunk: it
+                    // joins the block's last row, and fma(0, z, acc) == acc exactly (z finite,
+                    // acc never -0 since every chain starts at +0)
+                    if (ent.size() & 1) ent.push_back(make_int2(c * ZC * ZROW, 0));
+                }
+                for (int e = 4 * H; e < 4 * H + 4; ++e) o[e] = int32_t(ent.size());
+                // stage capacity: the largest 16-unit (and 8-unit) span of this chunk
+                for (int kb8 = 0; kb8 < H / 8; ++kb8) {
+                    const int span = (H % 16 == 0 && kb8 % 2 == 0) ? 2 : 1;
+                    ent_cap = std::max(ent_cap, o[std::min(kb8 + span, H / 8) * 32] - o[kb8 * 32]);
+                }
+            }
+        }
+        if (ent.size() > size_t(INT32_MAX)) return SPCONV_ERR_UNSUPPORTED;
+        if (ent.empty()) ent.push_back(make_int2(0, 0));
+    }
     spconv_lstm_s *p = new (std::nothrow) spconv_lstm_s;
     if (!p) return SPCONV_ERR_OOM;
-    p->L = L; p->D = D; p->H = H; p->device = device; p->nnz = nnz;
+    p->L = L; p->D = D; p->H = H; p->device = device; p->nnz = nnz; p->nzc = nzc; p->ent_cap = ent_cap + 2;
     auto up = [&](auto **dst, const auto &src) -> int {
         const size_t bytes = sizeof(src[0]) * std::max<size_t>(src.size(), 1);
         if (cudaMalloc(reinterpret_cast<void **>(dst), bytes) != cudaSuccess) {
@@ -305,7 +506,7 @@ int spconv_lstm_create(spconv_lstm_t *plan, int L, int D, int H, const int32_t *
         return SPCONV_OK;
     };
     if ((st = up(&p->d_rowptr, rp)) || (st = up(&p->d_colidx, ci)) || (st = up(&p->d_values, vv)) ||
-        (st = up(&p->d_bias, bb))) {
+        (st = up(&p->d_bias, bb)) || (!offs.empty() && ((st = up(&p->d_off, offs)) || (st = up(&p->d_ent, ent))))) {
         free_lstm(p);
         return st;
     }
@@ -365,9 +566,39 @@ int spconv_lstm_forward(spconv_lstm_t plan, int T, int B, const float *x, float 
     a.rowptr = p->d_rowptr; a.colidx = p->d_colidx; a.values = p->d_values; a.bias = p->d_bias;
     a.xT = xT; a.hist = hist; a.cst = cst;
     a.L = L; a.D = D; a.H = H; a.T = T; a.B = B; a.nbc = (B + 63) / 64;
+    // B >= 32: the z-staged kernel when rows are 16-byte strided (else one warp per row set)
+    const char *kenv = std::getenv("SPCONV_LSTM_KERNEL"); // A/B tooling and tests
+    const bool rowwarp = kenv && std::strcmp(kenv, "rowwarp") == 0;
+    bool staged = !rowwarp && B >= 32 && B % 4 == 0 && H % 8 == 0 && p->d_off;
+    // dynamic shared memory: 2 stages x (z tile + entry buffer + row offsets)
+    const size_t zent = size_t(ZC) * ZROW + size_t(p->ent_cap) * 8;
+    const size_t smem16 = 2 * (zent + (4 * 16 + 4) * 4), smem8 = 2 * (zent + (4 * 8 + 4) * 4);
+    if (staged) {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+        if (smem16 > size_t(optin) ||
+            cudaFuncSetAttribute(lstm_cells_staged_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem16)) != cudaSuccess ||
+            cudaFuncSetAttribute(lstm_cells_staged_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem8)) != cudaSuccess) {
+            cudaGetLastError();
+            staged = false; // very dense layers: the one-warp-per-unit kernel
+        }
+    }
+    const char *wenv = std::getenv("SPCONV_LSTM_WPC"); // A/B tooling: 16 warps per CTA
+    const bool wpc16 = wenv && std::atoi(wenv) == 16;
+    StagedArgs sa;
+    sa.off = p->d_off; sa.ent = p->d_ent; sa.nzc = p->nzc; sa.ent_cap = p->ent_cap;
     auto launch = [&](int w, int l0, int ncell) {
         a.w = w; a.l0 = l0; a.ncell = ncell;
-        if (B >= 32) {
+        if (staged) {
+            sa.a = a;
+            // 8 warps per CTA (measured faster than 16 at the paper's size: more CTAs per SM)
+            if (wpc16 && H % 16 == 0)
+                lstm_cells_staged_kernel<16><<<ncell * (H / 16) * a.nbc, 512, smem16, s>>>(sa);
+            else
+                lstm_cells_staged_kernel<8><<<ncell * (H / 8) * a.nbc, 256, smem8, s>>>(sa);
+        } else if (B >= 32) {
             const int64_t threads = int64_t(ncell) * H * a.nbc * 32;
             lstm_cells_kernel<<<int((threads + 255) / 256), 256, 0, s>>>(a);
         } else {

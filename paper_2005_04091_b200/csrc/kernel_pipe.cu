@@ -72,6 +72,7 @@ struct PipeArgs {
     unsigned long long *sk_flag;      // [grid][gpc]: == epoch when slot (b, warp) is ready
     unsigned long long epoch;
     unsigned long long *trace; // debug (SPCONV_PIPE_TRACE): per CTA 8 timestamps, or null
+    int rev;                   // debug (SPCONV_PIPE_REV=1): CTA b does the work of CTA grid-1-b
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
+    const int bid = a.rev ? int(gridDim.x) - 1 - int(blockIdx.x) : int(blockIdx.x); // work index
     const int ns = a.nstage;
     unsigned long long *tr = a.trace ? a.trace + size_t(blockIdx.x) * 8 : nullptr;
     if (tr && threadIdx.x == 0) {
@@ -328,14 +330,14 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         if (a.sk) {
             const int C = a.C;
             const int64_t tot = int64_t(nunits) * C;
-            const int64_t s0 = tot * blockIdx.x / gridDim.x, e0 = tot * (blockIdx.x + 1) / gridDim.x;
+            const int64_t s0 = tot * bid / gridDim.x, e0 = tot * (bid + 1) / gridDim.x;
             if (e0 % C) { q.hc = int(e0 % C); q.uh = int(e0 / C); q.hA = (q.hc + a.cc - 1) / a.cc; }
             if (s0 % C) { q.tcs = int(s0 % C); q.ut = int(s0 / C); q.tc0 = q.tcs / a.cc; q.tC = nch - q.tc0; }
             q.uf0 = int((s0 + C - 1) / C);
             q.nf = int(e0 / C) - q.uf0;
         } else {
-            q.uf0 = blockIdx.x;
-            q.nf = int(blockIdx.x) < nunits ? (nunits - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+            q.uf0 = bid;
+            q.nf = bid < nunits ? (nunits - 1 - bid) / int(gridDim.x) + 1 : 0;
         }
         q.total = q.hA + q.nf * nch + q.tC;
         sch = q;
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         if (kind == 2 && active) {
             // resume: wait for CTA b-1's parked accumulators of this warp (it parked
             // them before any other work, so this wait is normally already satisfied)
-            const size_t slot = size_t(blockIdx.x - 1) * a.gpc + warp;
+            const size_t slot = size_t(bid - 1) * a.gpc + warp;
             if (tr && threadIdx.x == 0) tr[3] = gtimer();
             unsigned long long f;
             do {
@@ -528,7 +530,7 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         if (!active) continue;
         if (kind == 1) {
             // park: the partial sums go to slot (b, warp) for CTA b+1
-            const size_t slot = size_t(blockIdx.x) * a.gpc + warp;
+            const size_t slot = size_t(bid) * a.gpc + warp;
             ulonglong2 *dst = a.sk_part + slot * (R * PT * SH / 2) * 32 + lane;
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -923,6 +925,8 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     if (const char *e = std::getenv("SPCONV_PIPE_SK")) a.sk = (e[0] == '1' && nunits > grid) ? 1 : 0;
     void *skw = nullptr;
     a.trace = nullptr;
+    a.rev = 0;
+    if (const char *e = std::getenv("SPCONV_PIPE_REV")) a.rev = e[0] == '1';
     const bool tracing = std::getenv("SPCONV_PIPE_TRACE") != nullptr;
     if (tracing && cudaMalloc(&a.trace, size_t(grid) * 64) == cudaSuccess) cudaMemsetAsync(a.trace, 0, size_t(grid) * 64, s);
     if (a.sk) {

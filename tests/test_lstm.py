@@ -73,6 +73,28 @@ def test_gpu_lstm_parity(L, D, H, T, B, d):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("L,D,H,T,B,d", [(2, 100, 48, 7, 36, 0.2), (3, 130, 96, 6, 128, 0.4),
+                                         (2, 64, 1024, 3, 64, 0.15)])
+def test_gpu_lstm_staged_kernel(L, D, H, T, B, d, monkeypatch):
+    """B >= 32 with 16-byte rows runs the z-staged kernel (chunks of 64 z rows in shared
+    memory; D=100 makes a chunk straddle the [input ; h] boundary, B=36 a partial batch
+    tile, B=128 two tiles, H=1024 with 2 cells the 16-warp CTA): parity with the oracle,
+    and bitwise equality with the one-warp-per-unit kernel (same fma chains)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _gpu_case(L, D, H, T, B, d, batch_sample=None if B <= 40 else [0, B // 2, B - 1])
+    from paper_2005_04091_b200.lstm import WAVEFRONT, SparseLSTM
+    layers, x = synthgen.make_lstm(L, D, H, d, T, B)
+    net = SparseLSTM(D, H, layers)
+    xt = torch.from_numpy(x).cuda()
+    h_staged = net(xt, WAVEFRONT).cpu().numpy()
+    monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")
+    h_row = net(xt, WAVEFRONT).cpu().numpy()
+    assert np.array_equal(h_staged.view(np.uint32), h_row.view(np.uint32))
+    net.close()
+
+
+@pytest.mark.gpu
 def test_gpu_lstm_paper_size_sampled():
     """PAPER.md L510 sizes (4 layers, T=100, H=1024, 15% density), B=64, oracle on a
     sample of batch columns (they are independent)."""
