@@ -126,8 +126,9 @@ __global__ void __launch_bounds__(256) lstm_cells_kernel(const CellArgs a) {
 // LDS.64 (z), two fma.  Rows' entries stay in ascending column order and chunks
 // ascend, so every gate is the same fma chain as in lstm_cells_kernel (bitwise
 // identical results).
-constexpr int ZC = 64;          // z rows per staged chunk
+constexpr int ZC = 64;          // z rows per staged chunk (32 and 3 stages measured slower)
 constexpr int ZROW = 64 * 4;    // bytes per staged z row (64 batch columns)
+constexpr int LSTM_NSTG = 2;    // cp.async stages in flight (3 measured slower: fewer CTAs per SM)
 
 struct StagedArgs {
     CellArgs a;
@@ -176,7 +177,7 @@ __device__ __forceinline__ void walk_row(const int2 *es, int j, int je, const un
 template <int WPC>
 __global__ void __launch_bounds__(WPC * 32) lstm_cells_staged_kernel(const StagedArgs sa) {
     const CellArgs &a = sa.a;
-    // dynamic smem: [2 stages][ZC * ZROW z bytes | ent_cap * 8 entry bytes | (4*WPC + 4) offsets]
+    // dynamic smem: [LSTM_NSTG stages][ZC * ZROW z bytes | ent_cap * 8 entry bytes | (4*WPC + 4) offsets]
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int NQ = 4 * WPC;                 // gate rows of the CTA
     const uint32_t ent_bytes = uint32_t(sa.ent_cap) * 8u;
@@ -219,16 +220,19 @@ __global__ void __launch_bounds__(WPC * 32) lstm_cells_staged_kernel(const Stage
 
     float acc[4][2] = {};
     const int w8 = warp >> 3, wl = warp & 7;    // 8-unit block within the CTA, unit within it
-    stage(0, 0);
+    // LSTM_NSTG-deep cp.async ring (empty commit groups keep the group count uniform)
+#pragma unroll
+    for (int s0 = 0; s0 < LSTM_NSTG - 1; ++s0) {
+        if (s0 < nch) stage(s0, s0);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     for (int c = 0; c < nch; ++c) {
-        if (c + 1 < nch) {
-            stage(c + 1, (c + 1) & 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
+        const int cn = c + LSTM_NSTG - 1;
+        if (cn < nch) stage(cn, cn % LSTM_NSTG);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(LSTM_NSTG - 1) : "memory");
         __syncthreads();
-        const unsigned char *sb = dsm + size_t(c & 1) * stage_bytes;
+        const unsigned char *sb = dsm + size_t(c % LSTM_NSTG) * stage_bytes;
         const int2 *es = reinterpret_cast<const int2 *>(sb + ZC * ZROW);
         const int32_t *so = reinterpret_cast<const int32_t *>(sb + ZC * ZROW + ent_bytes);
         // generic pointer such that zb + col * ZROW addresses row col - c * ZC of the tile
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(WPC * 32) lstm_cells_staged_kernel(const Stage
         walk_row(es, so[qb + 8] - eb, so[qb + 9] - eb, zb, acc[1][0], acc[1][1]);
         walk_row(es, so[qb + 16] - eb, so[qb + 17] - eb, zb, acc[2][0], acc[2][1]);
         walk_row(es, so[qb + 24] - eb, so[qb + 25] - eb, zb, acc[3][0], acc[3][1]);
-        __syncthreads(); // buffer c & 1 is refilled by the next iteration's stage()
+        __syncthreads(); // buffer c % LSTM_NSTG is refilled by a later iteration's stage()
     }
     float gate[4][2];
 #pragma unroll
@@ -570,9 +574,9 @@ int spconv_lstm_forward(spconv_lstm_t plan, int T, int B, const float *x, float 
     const char *kenv = std::getenv("SPCONV_LSTM_KERNEL"); // A/B tooling and tests
     const bool rowwarp = kenv && std::strcmp(kenv, "rowwarp") == 0;
     bool staged = !rowwarp && B >= 32 && B % 4 == 0 && H % 8 == 0 && p->d_off;
-    // dynamic shared memory: 2 stages x (z tile + entry buffer + row offsets)
+    // dynamic shared memory: LSTM_NSTG stages x (z tile + entry buffer + row offsets)
     const size_t zent = size_t(ZC) * ZROW + size_t(p->ent_cap) * 8;
-    const size_t smem16 = 2 * (zent + (4 * 16 + 4) * 4), smem8 = 2 * (zent + (4 * 8 + 4) * 4);
+    const size_t smem16 = LSTM_NSTG * (zent + (4 * 16 + 4) * 4), smem8 = LSTM_NSTG * (zent + (4 * 8 + 4) * 4);
     if (staged) {
         int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
