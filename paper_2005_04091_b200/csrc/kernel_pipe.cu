@@ -359,6 +359,13 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // Programmatic dependent launch: let the next launch on the stream start its
+    // prologue on SMs this grid frees, and wait here for the previous grid (whose
+    // outputs x may be, and whose stream-K workspace this launch reuses) to finish.
+    // Without the launch attribute both are no-ops.  Only plan tables (immutable)
+    // were read above.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     auto fill = [&](int kk, int s) {
         int u, ch;
@@ -671,6 +678,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
+// SPCONV_PDL=0 launches without programmatic dependent launch (A/B tooling)
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("SPCONV_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG, int EPI = 0>
 cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size_t smem, cudaStream_t s) {
     auto kern = pipe_kernel<R, PT, PS, FUSED, XS, DISP, STG, EPI>;
@@ -683,8 +699,17 @@ cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size
         if (e != cudaSuccess) return e;
         __atomic_store_n(&done, smem, __ATOMIC_RELEASE);
     }
-    kern<<<grid, 32 * a.gpc, smem, s>>>(map, a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(32 * a.gpc));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, map, a);
 }
 
 // Shared-memory wavefronts of one warp-wide window row load (LDS.128 at the
@@ -923,7 +948,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.sk = 0; a.sk_part = nullptr; a.sk_flag = nullptr; a.epoch = 0;
     if (nunits > grid && nunits % grid != 0 && nunits < 16 * int64_t(grid)) a.sk = 1;
     if (const char *e = std::getenv("SPCONV_PIPE_SK")) a.sk = (e[0] == '1' && nunits > grid) ? 1 : 0;
-    void *skw = nullptr;
+    void *skw = nullptr, *sk_async = nullptr;
     a.trace = nullptr;
     a.rev = 0;
     if (const char *e = std::getenv("SPCONV_PIPE_REV")) a.rev = e[0] == '1';
@@ -934,11 +959,47 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         const int qn = p.R * g.T * g.S / 4;
         const size_t part_bytes = size_t(grid) * p.gpc * qn * 32 * sizeof(ulonglong2);
         const size_t flag_bytes = size_t(grid) * p.gpc * sizeof(unsigned long long);
-        keep_pool_cached();
-        cudaError_t e = cudaMallocAsync(&skw, part_bytes + flag_bytes, s);
-        if (e != cudaSuccess) {
-            if (xp) cudaFreeAsync(xp, s);
-            return e;
+        // one workspace per (plan, stream), kept: launches on one stream are ordered
+        // (griddepcontrol.wait), launches on different streams never share one.  Under
+        // stream capture a stream-ordered allocation is used instead (capturable).
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        if (cap != cudaStreamCaptureStatusNone) {
+            keep_pool_cached();
+            cudaError_t e = cudaMallocAsync(&skw, part_bytes + flag_bytes, s);
+            if (e != cudaSuccess) {
+                if (xp) cudaFreeAsync(xp, s);
+                return e;
+            }
+            sk_async = skw;
+        } else {
+            Plan &mp = const_cast<Plan &>(p);
+            std::lock_guard<std::mutex> lk(mp.sk_mu);
+            std::pair<void *, size_t> *ws = nullptr;
+            for (auto &w : mp.sk_ws)
+                if (w.first == s) ws = &w.second;
+            if (!ws) {
+                mp.sk_ws.push_back({s, {nullptr, 0}});
+                ws = &mp.sk_ws.back().second;
+            }
+            if (ws->second < part_bytes + flag_bytes) {
+                if (ws->first) {
+                    // the old buffer may still be in use by earlier launches on s
+                    cudaStreamSynchronize(s);
+                    cudaFree(ws->first);
+                    ws->first = nullptr;
+                    ws->second = 0;
+                }
+                cudaError_t e = cudaMalloc(&ws->first, part_bytes + flag_bytes);
+                if (e != cudaSuccess) {
+                    if (xp) cudaFreeAsync(xp, s);
+                    return e;
+                }
+                ws->second = part_bytes + flag_bytes;
+                // flags start at 0 (never equal to an epoch)
+                cudaMemsetAsync(static_cast<char *>(ws->first) + part_bytes, 0, flag_bytes, s);
+            }
+            skw = ws->first;
         }
         a.sk_part = reinterpret_cast<ulonglong2 *>(skw);
         a.sk_flag = reinterpret_cast<unsigned long long *>(static_cast<char *>(skw) + part_bytes);
@@ -982,8 +1043,8 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         }
         cudaFree(a.trace);
     }
-    if (skw) {
-        cudaError_t e2 = cudaFreeAsync(skw, s);
+    if (sk_async) {
+        cudaError_t e2 = cudaFreeAsync(sk_async, s);
         if (err == cudaSuccess) err = e2;
     }
     if (xp) {

@@ -82,6 +82,7 @@ void free_plan(Plan *p) {
     cudaFree(p->d_stream);
     cudaFree(p->d_chunk_start);
     cudaFree(p->d_stream2);
+    for (auto &w : p->sk_ws) cudaFree(w.second.first);
     cudaFree(p->d_xbuf);
     cudaFree(p->d_ybuf);
     cudaFree(p->d_abuf);

@@ -95,6 +95,10 @@ struct Plan {
     float *d_xbuf = nullptr, *d_ybuf = nullptr;
     int32_t *d_abuf = nullptr;
     size_t xbuf_elems = 0, ybuf_elems = 0;
+    // stream-K workspaces of the pipe kernel, one per stream (kept across calls so
+    // consecutive launches are adjacent in the stream: programmatic dependent launch)
+    std::mutex sk_mu;
+    std::vector<std::pair<cudaStream_t, std::pair<void *, size_t>>> sk_ws;
     cudaStream_t host_stream = nullptr;    // host -> device copies
     static constexpr int HOST_KSTREAMS = 3;
     cudaStream_t host_kstream[HOST_KSTREAMS] = {}; // forwards of spconv_forward_host (chunks round-robin)
