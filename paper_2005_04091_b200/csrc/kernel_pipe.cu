@@ -964,7 +964,15 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         // stream capture a stream-ordered allocation is used instead (capturable).
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(s, &cap);
-        if (cap != cudaStreamCaptureStatusNone) {
+        bool cached = cap == cudaStreamCaptureStatusNone;
+        if (cached) { // at most 8 cached streams per plan (each ~19 MB on c2); others allocate per call
+            Plan &mp = const_cast<Plan &>(p);
+            std::lock_guard<std::mutex> lk(mp.sk_mu);
+            bool known = false;
+            for (auto &w : mp.sk_ws) known |= w.first == s;
+            cached = known || mp.sk_ws.size() < 8;
+        }
+        if (!cached) {
             keep_pool_cached();
             cudaError_t e = cudaMallocAsync(&skw, part_bytes + flag_bytes, s);
             if (e != cudaSuccess) {

@@ -625,6 +625,15 @@ int spconv_forward_host(spconv_plan_t plan, int N, const float *x_host, float *y
     if (const char *e = std::getenv("SPCONV_HOST_CHUNKS")) nchunk = std::atoi(e); // A/B tooling
     nchunk = std::max(1, std::min({nchunk, N, Plan::MAX_HOST_CHUNKS}));
     int32_t *dam = (fused && argmax_host) ? p->d_abuf : nullptr;
+    // on an error after the first enqueue, drain the streams before returning so no
+    // copy into or out of the caller's host buffers is still in flight
+    auto drain = [&](int st) {
+        cudaStreamSynchronize(p->host_stream);
+        for (cudaStream_t ks : p->host_kstream) cudaStreamSynchronize(ks);
+        cudaStreamSynchronize(p->host_ostream);
+        cudaGetLastError();
+        return st;
+    };
     for (int i = 0, n0 = 0; i < nchunk; ++i) {
         const int n1 = int(int64_t(N) * (i + 1) / nchunk), nb = n1 - n0;
         const size_t xo = size_t(n0) * xper, yo = size_t(n0) * yper;
@@ -633,17 +642,17 @@ int spconv_forward_host(spconv_plan_t plan, int N, const float *x_host, float *y
                             p->host_stream) != cudaSuccess ||
             cudaEventRecord(p->host_ev_in[i], p->host_stream) != cudaSuccess ||
             cudaStreamWaitEvent(ks, p->host_ev_in[i], 0) != cudaSuccess)
-            return SPCONV_ERR_CUDA;
+            return drain(SPCONV_ERR_CUDA);
         int st = run(plan, nb, p->d_xbuf + xo, p->d_ybuf + yo, dam ? dam + yo : nullptr, fused != 0, ks);
-        if (st) return st;
+        if (st) return drain(st);
         if (cudaEventRecord(p->host_ev_k[i], ks) != cudaSuccess ||
             cudaStreamWaitEvent(p->host_ostream, p->host_ev_k[i], 0) != cudaSuccess ||
             cudaMemcpyAsync(y_host + yo, p->d_ybuf + yo, size_t(nb) * yper * 4, cudaMemcpyDeviceToHost,
                             p->host_ostream) != cudaSuccess)
-            return SPCONV_ERR_CUDA;
+            return drain(SPCONV_ERR_CUDA);
         if (dam && cudaMemcpyAsync(argmax_host + yo, dam + yo, size_t(nb) * yper * 4, cudaMemcpyDeviceToHost,
                                    p->host_ostream) != cudaSuccess)
-            return SPCONV_ERR_CUDA;
+            return drain(SPCONV_ERR_CUDA);
         n0 = n1;
     }
     // the copy-out stream waited on every forward, each of which waited on its copy-in
