@@ -33,7 +33,7 @@ import os
 import sys
 
 # (R, T, S) variants instantiated by kernel_pipe.cu
-VARIANTS = [(4, 4, 8), (4, 8, 4)]
+VARIANTS = [(4, 4, 8), (4, 8, 4), (4, 4, 4)]
 MASK_VARIANTS = [(4, 8, 4)]
 # per-case entry load: one 16-byte load (ptxas hoists it and copies the value) or
 # two loads (value, next case) that need no copies but add a shared-memory op
