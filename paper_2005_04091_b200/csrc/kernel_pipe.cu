@@ -724,7 +724,7 @@ int window_wavefronts(const PipeGeometry &g, int pitch) {
         const int li = l < g.lanes ? l : 0;
         const int im = li / per_img, rem = li % per_img;
         const int tyl = rem / g.tiles_x, tx = rem % g.tiles_x;
-        addr[l] = (im * g.rs + tyl * PT) * pitch + tx * PS; // words
+        addr[l] = (im * g.cc * g.rs + tyl * PT) * pitch + tx * PS; // words (slot im of the stage)
     }
     int total = 0;
     for (int pass = 0; pass < 2; ++pass) {
@@ -802,10 +802,16 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
     g.lanes = g.ipb * g.tr * g.tiles_x;
     g.blocks_y = g.band ? 1 : (g.tiles_y + g.tr - 1) / g.tr;
     g.rs = PT * g.tr + 2;
+    g.cc = p.pipe_cc;
     // smem columns read: window of the last tile ends at 4*(tiles_x-1) + 5
     const int need = ((PS * g.tiles_x + 2) + 3) & ~3;
     int best = need, best_wf = 1 << 30;
     for (int cand = need; cand <= need + 32; cand += 4) {
+        // band mode stages every band with its own TMA box into slot b of the stage:
+        // slots must start on 128-byte boundaries (the tensor-copy destination
+        // alignment), i.e. cc * rs * pitch words must be a multiple of 32 (a pitch
+        // multiple of 16 words always qualifies, and the range holds two)
+        if (g.band && (g.cc * g.rs * cand) % 32 != 0) continue;
         const int wf = window_wavefronts(g, cand);
         if (wf < best_wf) {
             best_wf = wf;
@@ -813,9 +819,9 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
         }
     }
     g.pitch = best;
+    if (g.band && (g.cc * g.rs * g.pitch) % 32 != 0) return; // (unreachable: see the search)
     if (tma && (g.pitch > 256 || g.rs > 256)) return;
     if (mode == 0 && (p.W * 4) % 16 != 0) return;
-    g.cc = p.pipe_cc;
     g.nchunks = (p.C + g.cc - 1) / g.cc;
     g.in_words = g.ipb * g.cc * g.rs * g.pitch;
     g.in_pad = (g.in_words * 4 + 127) & ~127;

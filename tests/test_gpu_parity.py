@@ -492,3 +492,41 @@ def test_resize_then_fused_block(hw_in):
         rp, ra = oracle.fused_f32(rr, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
         assert np.array_equal(bits(p.cpu().numpy()), bits(rp)) and np.array_equal(am.cpu().numpy(), ra)
         layer.close()
+
+
+# ---------------------------------------------------------------- randomised shapes
+def test_random_shapes_bitwise_vs_oracle():
+    """60 seeded random layers (N, C, H, W, F, density, bias) through AUTO and every
+    kernel that accepts them (pipe needs K = 3, stride 1, pad 1 and W <= 124; tiled
+    K = 3): conv and fused outputs bitwise equal to the oracle, argmax exact.  Shapes
+    are drawn to cross tile, band, channel-stage and group-set boundaries."""
+    from paper_2005_04091_b200 import SparseConv2d
+    from paper_2005_04091_b200.spconv import SpconvError
+    rng = np.random.default_rng(20050409)
+    for i in range(60):
+        N = int(rng.integers(1, 6))
+        C = int(rng.integers(1, 40))
+        H = int(rng.integers(1, 40))
+        W = int(rng.choice([int(rng.integers(1, 40)), 4 * int(rng.integers(1, 31))]))
+        F = int(rng.integers(1, 70))
+        d = float(rng.choice([0.05, 0.2, 0.5, 1.0]))
+        seed = 9000 + 10 * i
+        csr = synthgen.make_csr(F, C, 3, d, seed, seed + 1)
+        xh = synthgen.make_input((N, C, H, W), seed + 2)
+        b = synthgen.make_bias(F, seed + 3) if i % 2 else None
+        ref = oracle.conv_f32(xh, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b)
+        fused_ref = oracle.fused_f32(xh, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b) if H >= 2 and W >= 2 else None
+        x = torch.from_numpy(xh).cuda()
+        for kernel in ("auto", "pipe", "tiled"):
+            try:
+                layer = SparseConv2d(C, H, W, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b, kernel=kernel)
+            except SpconvError as e:
+                assert e.status == -4, (i, kernel, e)  # unsupported shape for this kernel only
+                continue
+            y = layer(x).cpu().numpy()
+            assert np.array_equal(bits(y), bits(ref)), (i, kernel, N, C, H, W, F, d)
+            if fused_ref is not None:
+                p, am = layer.fused_relu_maxpool(x)
+                assert np.array_equal(bits(p.cpu().numpy()), bits(fused_ref[0])), (i, kernel)
+                assert np.array_equal(am.cpu().numpy(), fused_ref[1]), (i, kernel)
+            layer.close()
