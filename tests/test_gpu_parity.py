@@ -530,3 +530,54 @@ def test_random_shapes_bitwise_vs_oracle():
                 assert np.array_equal(bits(p.cpu().numpy()), bits(fused_ref[0])), (i, kernel)
                 assert np.array_equal(am.cpu().numpy(), fused_ref[1]), (i, kernel)
             layer.close()
+
+
+def test_random_epilogues_and_generic_shapes_bitwise_vs_oracle():
+    """Seeded random layers through the block epilogues (ReLU, residual add, both, in
+    place) on AUTO, and random K / stride / pad through the generic kernel: bitwise
+    equal to the oracle (conv_ex_f32 = ReLU((conv + b) + residual), R1)."""
+    from paper_2005_04091_b200 import SparseConv2d
+    rng = np.random.default_rng(5140)
+    for i in range(30):
+        N, C, H = int(rng.integers(1, 4)), int(rng.integers(1, 33)), int(rng.integers(2, 30))
+        W = int(rng.choice([int(rng.integers(2, 30)), 4 * int(rng.integers(1, 20))]))
+        F, d = int(rng.integers(1, 50)), float(rng.choice([0.1, 0.3, 1.0]))
+        seed = 12000 + 10 * i
+        csr = synthgen.make_csr(F, C, 3, d, seed, seed + 1)
+        xh = synthgen.make_input((N, C, H, W), seed + 2)
+        b = synthgen.make_bias(F, seed + 3)
+        res = synthgen.make_input((N, F, H, W), seed + 4)
+        layer = SparseConv2d(C, H, W, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b)
+        x = torch.from_numpy(xh).cuda()
+        r = torch.from_numpy(res).cuda()
+        for relu, use_res in ((True, False), (False, True), (True, True)):
+            y = layer.forward_ex(x, relu=relu, residual=r if use_res else None).cpu().numpy()
+            ref = oracle.conv_ex_f32(xh, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b,
+                                     residual=res if use_res else None, relu=relu)
+            assert np.array_equal(bits(y), bits(ref)), (i, relu, use_res)
+        # in place: y = ReLU(conv + b + y)
+        y = r.clone()
+        layer.forward_ex(x, relu=True, residual=y, out=y)
+        ref = oracle.conv_ex_f32(xh, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b, residual=res, relu=True)
+        assert np.array_equal(bits(y.cpu().numpy()), bits(ref)), (i, "in place")
+        layer.close()
+    for i in range(30):
+        K = int(rng.choice([1, 3, 5, 7]))
+        s, p = int(rng.integers(1, 3)), int(rng.integers(0, K))
+        N, C, F = int(rng.integers(1, 4)), int(rng.integers(1, 20)), int(rng.integers(1, 20))
+        H, W = int(rng.integers(K, K + 20)), int(rng.integers(K, K + 20))
+        d = float(rng.choice([0.2, 0.6, 1.0]))
+        seed = 13000 + 10 * i
+        csr = synthgen.make_csr(F, C, K, d, seed, seed + 1)
+        xh = synthgen.make_input((N, C, H, W), seed + 2)
+        b = synthgen.make_bias(F, seed + 3) if i % 2 else None
+        layer = SparseConv2d(C, H, W, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b, kernel="generic")
+        x = torch.from_numpy(xh).cuda()
+        y = layer(x).cpu().numpy()
+        ref = oracle.conv_f32(xh, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b)
+        assert np.array_equal(bits(y), bits(ref)), (i, K, s, p)
+        if layer.Ho >= 2 and layer.Wo >= 2:
+            pp, am = layer.fused_relu_maxpool(x)
+            rp, ra = oracle.fused_f32(xh, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b)
+            assert np.array_equal(bits(pp.cpu().numpy()), bits(rp)) and np.array_equal(am.cpu().numpy(), ra), i
+        layer.close()

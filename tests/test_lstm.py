@@ -101,3 +101,33 @@ def test_gpu_lstm_paper_size_sampled():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     _gpu_case(4, 1024, 1024, 100, 64, 0.15, batch_sample=[0, 31, 63])
+
+
+@pytest.mark.gpu
+def test_gpu_lstm_random_shapes(monkeypatch):
+    """Seeded random LSTM shapes across the three cell kernels (lanes-over-nonzeros for
+    B < 32, z-staged for B >= 32 with B % 4 == 0 and H % 8 == 0, one warp per unit
+    otherwise): wavefront == sequential bitwise, staged == one-warp-per-unit bitwise,
+    and the float64 oracle within the R3 tolerance on sampled batch columns."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2005_04091_b200.lstm import WAVEFRONT, SparseLSTM
+    rng = np.random.default_rng(1510)
+    for i in range(8):
+        L = int(rng.integers(1, 4))
+        D = int(rng.integers(1, 150))
+        H = int(rng.choice([8, 16, 24, 40, 64, 13]))
+        T = int(rng.integers(1, 8))
+        B = int(rng.choice([1, 5, 32, 36, 44, 64, 66, 96]))
+        d = float(rng.choice([0.05, 0.15, 0.5]))
+        _gpu_case(L, D, H, T, B, d, batch_sample=None if B <= 8 else [0, B // 2, B - 1])
+        layers, x = synthgen.make_lstm(L, D, H, d, T, B)
+        net = SparseLSTM(D, H, layers)
+        xt = torch.from_numpy(x).cuda()
+        h_default = net(xt, WAVEFRONT).cpu().numpy()
+        monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")
+        h_row = net(xt, WAVEFRONT).cpu().numpy()
+        monkeypatch.delenv("SPCONV_LSTM_KERNEL")
+        if B >= 32:
+            assert np.array_equal(h_default.view(np.uint32), h_row.view(np.uint32)), (i, L, D, H, T, B, d)
+        net.close()
