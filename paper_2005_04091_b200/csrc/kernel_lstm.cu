@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) lstm_cells_kernel(const CellArgs a) {
 // LDS.64 (z), two fma.  Rows' entries stay in ascending column order and chunks
 // ascend, so every gate is the same fma chain as in lstm_cells_kernel (bitwise
 // identical results).
-constexpr int ZC = 64;          // z rows per staged chunk (32 and 3 stages measured slower)
+constexpr int ZC = 128;         // z rows per staged chunk (measured: 32 and 64 slower; per-chunk overhead)
 constexpr int ZROW = 64 * 4;    // bytes per staged z row (64 batch columns)
 constexpr int LSTM_NSTG = 2;    // cp.async stages in flight (3 measured slower: fewer CTAs per SM)
 
@@ -606,16 +606,17 @@ int spconv_lstm_forward(spconv_lstm_t plan, int T, int B, const float *x, float 
             staged = false; // very dense layers: the one-warp-per-unit kernel
         }
     }
-    const char *wenv = std::getenv("SPCONV_LSTM_WPC"); // A/B tooling: 16 warps per CTA
-    const bool wpc16 = wenv && std::atoi(wenv) == 16;
+    const char *wenv = std::getenv("SPCONV_LSTM_WPC"); // A/B tooling: force 8 or 16 warps per CTA
+    const int wpc = wenv ? std::atoi(wenv) : 0;
     StagedArgs sa;
     sa.off = p->d_off; sa.ent = p->d_ent; sa.nzc = p->nzc; sa.ent_cap = p->ent_cap;
     auto launch = [&](int w, int l0, int ncell) {
         a.w = w; a.l0 = l0; a.ncell = ncell;
         if (staged) {
             sa.a = a;
-            // 8 warps per CTA (measured faster than 16 at the paper's size: more CTAs per SM)
-            if (wpc16 && H % 16 == 0)
+            // 16 warps per CTA (half the z staging per gate row) when that still gives a
+            // CTA per SM (paper size, wavefront: 12.5 -> 9.5 ms); else 8 (sequential)
+            if (H % 16 == 0 && wpc != 8 && (wpc == 16 || int64_t(ncell) * (H / 16) * a.nbc >= 148))
                 lstm_cells_staged_kernel<16><<<ncell * (H / 16) * a.nbc, 512, smem16, s>>>(sa);
             else
                 lstm_cells_staged_kernel<8><<<ncell * (H / 8) * a.nbc, 256, smem8, s>>>(sa);
