@@ -20,4 +20,10 @@ for c in c2 c3 c4_80 c5; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:pipe_kernel -s 3 -c 1 \
      -o gpurun_out/full_$c -f python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/full_$c.log 2>&1
 done
+timeout 600 python scripts/lstm_bench.py --batch 64 --reps 10 > gpurun_out/lstm_b64.jsonl 2>&1
+timeout 600 python scripts/lstm_bench.py --batch 1 --reps 10 > gpurun_out/lstm_b1.jsonl 2>&1
+for tool in memcheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool python scripts/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "rc=$?" >> gpurun_out/sanitize_$tool.log
+done
 echo done

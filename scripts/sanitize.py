@@ -59,6 +59,15 @@ def main():
     print("lstm", "ok" if ok else "MISMATCH")
     good &= ok
     net.close()
+    # batch >= 32: the z-staged kernel (cp.async ring, entries staged per chunk)
+    layers, xl = synthgen.make_lstm(2, 100, 48, 0.2, 3, 36)
+    net = SparseLSTM(100, 48, layers)
+    hw = net(torch.from_numpy(xl).cuda(), WAVEFRONT).cpu().numpy()
+    hs = net(torch.from_numpy(xl).cuda(), SEQUENTIAL).cpu().numpy()
+    ok = np.array_equal(bits(hw), bits(hs)) and np.abs(hw - oracle.lstm_f64(xl, layers, 48)).max() < 1e-5
+    print("lstm staged", "ok" if ok else "MISMATCH")
+    good &= ok
+    net.close()
     torch.cuda.synchronize()
     sys.exit(0 if good else 1)
 
