@@ -581,3 +581,28 @@ def test_random_epilogues_and_generic_shapes_bitwise_vs_oracle():
             rp, ra = oracle.fused_f32(xh, F, K, s, p, csr.rowptr, csr.colidx, csr.values, b)
             assert np.array_equal(bits(pp.cpu().numpy()), bits(rp)) and np.array_equal(am.cpu().numpy(), ra), i
         layer.close()
+
+
+@pytest.mark.parametrize("env", [{"SPCONV_PIPE_BANDS": "0"}, {"SPCONV_PIPE_CC": "3"}, {"SPCONV_PIPE_CC": "5"},
+                                 {"SPCONV_PIPE_CC": "7", "SPCONV_PIPE_STAGING": "pad"}])
+def test_pipe_tuning_options_keep_the_bits(env, monkeypatch):
+    """The A/B tuning options of the pipelined kernel change only the schedule:
+    whole-image units instead of bands, and odd channels-per-stage (band slots then
+    need a pitch that keeps them 128-byte aligned for TMA) -- bits equal to the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _check_full(synthgen.CONFIGS["c2"], "pipe", False, N=3)
+    _check_full(synthgen.CONFIGS["c3"], "pipe", True, N=2)
+
+
+def test_forward_host_chunk_counts(monkeypatch):
+    """spconv_forward_host with 1, 5 and 16 pipelined chunks: the same bits."""
+    cfg = synthgen.CONFIGS["c2"].with_batch(7)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    layer = _layer(cfg, c, None, "auto")
+    ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, None)
+    for k in ("1", "5", "16"):
+        monkeypatch.setenv("SPCONV_HOST_CHUNKS", k)
+        assert np.array_equal(bits(layer.forward_host(L.x)), bits(ref)), k
+    layer.close()

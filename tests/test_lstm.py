@@ -95,6 +95,25 @@ def test_gpu_lstm_staged_kernel(L, D, H, T, B, d, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("wpc", ["8", "16"])
+def test_gpu_lstm_staged_cta_sizes(wpc, monkeypatch):
+    """8- and 16-warp CTAs of the staged kernel (SPCONV_LSTM_WPC) give the same bits."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2005_04091_b200.lstm import WAVEFRONT, SparseLSTM
+    layers, x = synthgen.make_lstm(2, 70, 64, 0.2, 4, 40)
+    net = SparseLSTM(70, 64, layers)
+    xt = torch.from_numpy(x).cuda()
+    monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")
+    ref = net(xt, WAVEFRONT).cpu().numpy()
+    monkeypatch.delenv("SPCONV_LSTM_KERNEL")
+    monkeypatch.setenv("SPCONV_LSTM_WPC", wpc)
+    h = net(xt, WAVEFRONT).cpu().numpy()
+    assert np.array_equal(h.view(np.uint32), ref.view(np.uint32))
+    net.close()
+
+
+@pytest.mark.gpu
 def test_gpu_lstm_paper_size_sampled():
     """PAPER.md L510 sizes (4 layers, T=100, H=1024, 15% density), B=64, oracle on a
     sample of batch columns (they are independent)."""
