@@ -1,8 +1,8 @@
 """Generate dispatch2_gen.inc: the tap dispatcher of kernel_pipe.cu (v2 kernel).
 
 For one (row group, pipeline stage of input channels) a warp walks a
-shared-memory stream of 16-byte entries {v, v, case of the NEXT entry, 0}
-(the segment starts with a lead entry holding the first case).  Every tap
+shared-memory stream of 8-byte entries {v, case of the NEXT entry} (the
+segment starts with a lead entry holding the first case).  Every tap
 case = r*9 + ky*3 + kx selects the FMAs of one CSR nonzero on the thread's
 T x S output tile ("out[n][y][x] +=
 coeff * in[...]"):
@@ -18,9 +18,9 @@ issues T*S scalar FFMA.
 Dispatch is "threaded code" through one brx.idx jump table, software-
 pipelined: the case id of nonzero k+1 is already in a register when case k
 starts, so the jump-table load for k+1 (an indexed constant load) is issued
-at the top of case k and overlaps its FMAs; the tail of case k loads the
-VALUE of entry k+1 straight into the value register (its latency hides under
-the branch) and the case id of entry k+2.  Long case bodies (T*S FMAs) are
+at the top of case k and overlaps its FMAs; case k loads the case id of
+entry k+2 early and, after its FMAs, the VALUE of entry k+1 straight into the
+FMA operand register (its latency hides under the branch).  Long case bodies (T*S FMAs) are
 what hide the jump latency (scripts/probes/dispatch_probe.cu measures it).
 
 One walk covers all channels of a pipeline stage: case R*9 ("next channel")
@@ -35,11 +35,12 @@ import sys
 # (R, T, S) variants instantiated by kernel_pipe.cu
 VARIANTS = [(4, 4, 8), (4, 8, 4), (4, 4, 4)]
 MASK_VARIANTS = [(4, 8, 4)]
-# per-case entry load: one 16-byte load (ptxas hoists it and copies the value: 3
-# IMAD.MOV per case on the FMA pipe) or two loads (value straight into the FFMA2
-# operand at the end of the case, next case id early) with no copies -- measured
-# faster on B200 (A/B: c2 14.79 -> 15.13 TFLOP/s, c3 +0.3%, c5 +0.7%), the default
-SPLIT_LOADS = os.environ.get("SPCONV_GEN_SPLIT", "1") == "1"
+# Stream entries are 8 bytes {value (f32), case of the NEXT entry (u32)}: the value
+# is loaded straight into the FMA operand at the end of a case (FFMA2 takes it as a
+# broadcast .F32 operand), the next case id early -- no register copies.  (Measured
+# on B200: 16-byte {v, v, case, 0} entries with one load and register copies were
+# 2.3% slower on c2.)
+ENT = 8
 
 
 def gen(R: int, T: int, S: int) -> str:
@@ -58,19 +59,14 @@ def gen(R: int, T: int, S: int) -> str:
     def head():
         # case id of entry k+1 (it came with entry k): its jump-table load overlaps
         # this case's FMAs
-        return ["cvt.u32.u64 %%cn, %%kx;"]
+        return ["mov.b32 %%cn, %%cx;"]
 
     def tail():
-        # after the FMAs, entry k+1 = {v, v, case of k+2, 0}: the value lands
-        # straight in va (no register rotation copies); sp -> k+2
-        if SPLIT_LOADS:
-            return ["ld.shared.b64 %%va, [%%sp];",
-                    "ld.shared.u32 %%cx, [%%sp+8];",
-                    "cvt.u64.u32 %%kx, %%cx;",
-                    "add.u32 %%sp, %%sp, 16;",
-                    f"brx.idx.uni %%cn, $D{tag}_T;"]
-        return ["ld.shared.v2.b64 {%%va, %%kx}, [%%sp];",
-                "add.u32 %%sp, %%sp, 16;",
+        # after the FMAs, entry k+1 = {v, case of k+2}: the value lands straight in
+        # the operand register; sp -> entry k+2
+        return ["ld.shared.f32 %%vf, [%%sp];",
+                "ld.shared.u32 %%cx, [%%sp+4];",
+                f"add.u32 %%sp, %%sp, {ENT};",
                 f"brx.idx.uni %%cn, $D{tag}_T;"]
 
     P = f"%{nacc}"  # u32 shared-memory stream address, in/out
@@ -81,16 +77,18 @@ def gen(R: int, T: int, S: int) -> str:
     tag = f"R{R}T{T}S{S}"
     L = []
     L.append("{")
-    L.append(".reg .b64 %%va, %%kx;")  # (v, v) of the current entry, (case of the next, 0)
-    L.append(".reg .b32 %%cn, %%cx, %%sp, %%v1, %%vd, %%wa;")
+    L.append(".reg .b64 %%va;")  # (v, v): the FFMA2 operand (ptxas folds it into a .F32 broadcast)
+    L.append(".reg .f32 %%vf;")  # the current entry's value
+    L.append(".reg .b32 %%cn, %%cx, %%sp, %%wa;")
     L.append(".reg .f32 " + ", ".join(f"%%a{i}" for i in range(S)) + ", "
              + ", ".join(f"%%x{i}" for i in range(S + 2)) + ";")
     # P -> a lead entry whose case field is the first entry's case (the segment's
     # header entry, or a "next channel" marker when a walk starts mid-stage)
     L.append(f"mov.b32 %%sp, {P};")
-    L.append("ld.shared.u32 %%cn, [%%sp+8];")
-    L.append("ld.shared.v2.b64 {%%va, %%kx}, [%%sp+16];")
-    L.append("add.u32 %%sp, %%sp, 32;")
+    L.append("ld.shared.u32 %%cn, [%%sp+4];")
+    L.append(f"ld.shared.f32 %%vf, [%%sp+{ENT}];")
+    L.append(f"ld.shared.u32 %%cx, [%%sp+{ENT + 4}];")
+    L.append(f"add.u32 %%sp, %%sp, {2 * ENT};")
     L.append(f"$D{tag}_T: .branchtargets " + ", ".join(f"$D{tag}_{i}" for i in range(ncase + 2)) + ";")
     L.append(f"brx.idx.uni %%cn, $D{tag}_T;")
     for i in range(ncase):
@@ -99,11 +97,11 @@ def gen(R: int, T: int, S: int) -> str:
         L.append(f"$D{tag}_{i}:")
         L += head()
         if kx != 1:
+            L.append("mov.b64 %%va, {%%vf, %%vf};")
             for t in range(T):
                 for h in range(SH):
                     L.append(f"fma.rn.f32x2 {A(r, t, h)}, %%va, {X(t + ky, h + kx // 2)}, {A(r, t, h)};")
         else:
-            L.append("mov.b64 {%%v1, %%vd}, %%va;")
             for t in range(T):
                 row = t + ky
                 for j in range(PAIRS):
@@ -111,7 +109,7 @@ def gen(R: int, T: int, S: int) -> str:
                 for h in range(SH):
                     L.append(f"mov.b64 {{%%a{2 * h}, %%a{2 * h + 1}}}, {A(r, t, h)};")
                 for s in range(S):
-                    L.append(f"fma.rn.f32 %%a{s}, %%v1, %%x{s + 1}, %%a{s};")
+                    L.append(f"fma.rn.f32 %%a{s}, %%vf, %%x{s + 1}, %%a{s};")
                 for h in range(SH):
                     L.append(f"mov.b64 {A(r, t, h)}, {{%%a{2 * h}, %%a{2 * h + 1}}};")
         L += tail()

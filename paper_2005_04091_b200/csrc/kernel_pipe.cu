@@ -25,7 +25,7 @@
 //    waits for a slower one except on data.
 //  * Consumer (a5): per channel, load the 6x6 window (LDS.128 + LDS.64 per
 //    row), then run the threaded-code dispatcher of dispatch2_gen.inc over
-//    the warp's entries {v, v, case}: one brx.idx per nonzero, the jump
+//    the warp's entries {v, next case}: one brx.idx per nonzero, the jump
 //    target of nonzero k+1 and the entry of k+2 fetched while k's FMAs issue.
 //  * Epilogue (a6): + bias and store; or ReLU, 2x2 max and first-max argmax
 //    (the conv output is never written).
@@ -181,16 +181,16 @@ __device__ __forceinline__ void mask_walk(uint64_t (&acc)[R][PT][PS / 2], const 
 }
 
 // Index of the k-th (1-based) entry of a warp's stream segment whose case field
-// is the "next channel" marker (case id `marker`).  Entries are 16-byte {v, v,
-// case of the following entry, 0} behind a lead entry, so that index is the entry
-// BEFORE the marker: setting its case field to "end" ends the walk after channel
-// k-1, and the marker entry (index + 1) is a valid lead entry for a walk starting
-// at channel k.  Warp-cooperative (ballot over 32 entries at a time); the caller
-// asks for k < the stage's channel count, so the marker exists.
-__device__ __forceinline__ int find_marker(const uint4 *seg, int k, int lane, uint32_t marker) {
+// is the "next channel" marker (case id `marker`).  Entries are 8-byte {v, case of
+// the following entry} behind a lead entry, so that index is the entry BEFORE the
+// marker: setting its case field to "end" ends the walk after channel k-1, and the
+// marker entry (index + 1) is a valid lead entry for a walk starting at channel k.
+// Warp-cooperative (ballot over 32 entries at a time); the caller asks for k < the
+// stage's channel count, so the marker exists.
+__device__ __forceinline__ int find_marker(const uint2 *seg, int k, int lane, uint32_t marker) {
     int seen = 0;
     for (int base = 0;; base += 32) {
-        const unsigned m = __ballot_sync(0xffffffffu, seg[base + lane].z == marker);
+        const unsigned m = __ballot_sync(0xffffffffu, seg[base + lane].y == marker);
         const int c = __popc(m);
         if (seen + c >= k) {
             unsigned mm = m;
@@ -472,18 +472,18 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
                 uint64_t xw[PT + 2][PAIRS];
                 const unsigned char *wptr = stage + win_off;
                 if (cl0 > 0 || cl1 < ncl) { // warp-uniform, at most twice per CTA
-                    uint4 *seg = reinterpret_cast<uint4 *>(smem + size_t(s) * stage_bytes + a.in_pad + seg_off);
+                    uint2 *seg = reinterpret_cast<uint2 *>(smem + size_t(s) * stage_bytes + a.in_pad + seg_off);
                     if (cl1 < ncl) {
                         // end the walk after channel cl1 - 1: its marker becomes "end" (this
                         // warp's private copy of the segment; the refill overwrites it)
                         const int j = find_marker(seg, cl1, lane, 9u * R);
-                        if (lane == 0) seg[j].z = 9u * R + 1u;
+                        if (lane == 0) seg[j].y = 9u * R + 1u;
                         __syncwarp();
                     }
                     if (cl0 > 0) {
                         // start at channel cl0: the marker entry before it is the lead entry
                         const int j = find_marker(seg, cl0, lane, 9u * R);
-                        sp += uint32_t(j + 1) * 16u;
+                        sp += uint32_t(j + 1) * 8u;
                         wp += uint32_t(cl0) * ch_bytes;
                         wptr += size_t(cl0) * ch_bytes;
                     }

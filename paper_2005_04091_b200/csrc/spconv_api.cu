@@ -169,9 +169,9 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         // byte offsets (one per warp, 16-byte padded) then, per warp, for each channel
         // of the stage its group's nonzeros with case = (ky*3 + kx)*R + r, ascending
         // by case, followed by a "next channel" marker (case R*9) or, after the
-        // stage's last channel, an "end" marker (R*9+1).  Stored as 16-byte entries
-        // {v, v, case of the following entry, 0} behind a lead entry {0, 0, first
-        // case, 0} (gen_dispatch2.py).
+        // stage's last channel, an "end" marker (R*9+1).  Stored as 8-byte entries
+        // {v, case of the following entry} behind a lead entry {0, first case}
+        // (gen_dispatch2.py), two per 16-byte stream word.
         // Ascending case within a channel, channels in order: every output row's
         // taps are consumed in ascending colidx order (the FP32 contract).
         p->gpc = std::min(p->num_groups, 8);
@@ -263,7 +263,7 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                         }
                         // the walk order (case, value) of this warp's stage, then stored with
                         // each entry carrying the NEXT entry's case behind a lead entry, so the
-                        // dispatcher gets value k+1 and case k+2 with one 16-byte load
+                        // case id of k+2 is loaded while case k+1 is dispatched
                         std::vector<std::pair<uint32_t, uint32_t>> walk;
                         for (int c = c0; c < c1; ++c) {
                             if (g < p->num_groups) {
@@ -280,10 +280,16 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                             }
                             walk.push_back({c + 1 < c1 ? NEXT : END, 0u});
                         }
-                        out.push_back(make_uint4(0u, 0u, walk[0].first, 0u));
+                        // 8-byte entries {value, case of the next entry} behind a lead entry
+                        // {0, first case}, two per 16-byte stream word (a segment is padded
+                        // to a whole word)
+                        std::vector<uint2> ent;
+                        ent.push_back(make_uint2(0u, walk[0].first));
                         for (size_t k = 0; k < walk.size(); ++k)
-                            out.push_back(make_uint4(walk[k].second, walk[k].second,
-                                                     k + 1 < walk.size() ? walk[k + 1].first : END, 0u));
+                            ent.push_back(make_uint2(walk[k].second, k + 1 < walk.size() ? walk[k + 1].first : END));
+                        if (ent.size() & 1) ent.push_back(make_uint2(0u, END));
+                        for (size_t k = 0; k < ent.size(); k += 2)
+                            out.push_back(make_uint4(ent[k].x, ent[k].y, ent[k + 1].x, ent[k + 1].y));
                     }
                     std::memcpy(reinterpret_cast<char *>(out.data() + base), offs.data(), offs.size() * 4);
                     maxb = std::max(maxb, int((out.size() - base) * 16));
