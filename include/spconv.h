@@ -81,7 +81,7 @@ typedef struct spconv_plan_s *spconv_plan_t;
 
 typedef struct {
     int kernel;       /* SPCONV_KERNEL_*                                         */
-    int rows_per_group; /* tiled: output channels per register tile (0 = auto)   */
+    int rows_per_group; /* output channels per register tile (0 = auto): tiled 4|8, pipe 4|2 */
     int reserved[6];  /* must be zero                                           */
 } spconv_options_t;
 

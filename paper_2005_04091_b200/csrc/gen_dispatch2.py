@@ -33,7 +33,7 @@ import os
 import sys
 
 # (R, T, S) variants instantiated by kernel_pipe.cu
-VARIANTS = [(4, 4, 8), (4, 8, 4), (4, 4, 4)]
+VARIANTS = [(4, 4, 8), (4, 8, 4), (4, 4, 4), (2, 8, 4)]
 MASK_VARIANTS = [(4, 8, 4)]
 # Stream entries are 8 bytes {value (f32), case of the NEXT entry (u32)}: the value
 # is loaded straight into the FMA operand at the end of a case (FFMA2 takes it as a

@@ -46,6 +46,9 @@ namespace {
 
 constexpr int MAXSTAGE = 8;
 constexpr int MAX_GPC = 8;
+// R = 2 (DESIGN.md §7 "next" 1): half the accumulators, so 12 warps fit the register
+// file (<= 168 registers per thread) -- more warps to hide the per-nonzero dispatch
+constexpr int MAX_GPC_R2 = 12;
 
 struct PipeArgs {
     const float *x;
@@ -281,7 +284,7 @@ __device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
 // EPI (conv-only path): bit 0 = ReLU, bit 1 = add a residual tensor; the order is
 // y = ReLU((acc + bias) + residual), two FP32 adds (reading for NEXT-3).
 template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG, int EPI>
-__global__ void __launch_bounds__(32 * MAX_GPC, 1)
+__global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[MAXSTAGE], empty_bar[MAXSTAGE];
@@ -504,6 +507,8 @@ __global__ void __launch_bounds__(32 * MAX_GPC, 1)
                 // one walk over the stage's channels: taps, "next channel" (window reload), end
                 if constexpr (R == 4 && PT == 4 && PS == 8) {
                     SPC2_DISPATCH_R4T4S8(acc, xw, sp, wp, ch_bytes, row_bytes);
+                } else if constexpr (R == 2 && PT == 8 && PS == 4) {
+                    SPC2_DISPATCH_R2T8S4(acc, xw, sp, wp, ch_bytes, row_bytes);
                 } else {
                     static_assert(R == 4 && PT == 8 && PS == 4, "no dispatcher generated for this variant");
                     SPC2_DISPATCH_R4T8S4(acc, xw, sp, wp, ch_bytes, row_bytes);
@@ -1033,6 +1038,12 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         else if (epi == 1) { SPC_PIPE_MODES(4, 8, 4, false, 0, 1) }
         else if (epi == 2) { SPC_PIPE_MODES(4, 8, 4, false, 0, 2) }
         else { SPC_PIPE_MODES(4, 8, 4, false, 0, 3) }
+    } else if (p.R == 2 && g.T == 8 && g.S == 4 && p.pipe_dispatch == 0) {
+        if (fused) { SPC_PIPE_MODES(2, 8, 4, true, 0, 0) }
+        else if (epi == 0) { SPC_PIPE_MODES(2, 8, 4, false, 0, 0) }
+        else if (epi == 1) { SPC_PIPE_MODES(2, 8, 4, false, 0, 1) }
+        else if (epi == 2) { SPC_PIPE_MODES(2, 8, 4, false, 0, 2) }
+        else { SPC_PIPE_MODES(2, 8, 4, false, 0, 3) }
     }
 #undef SPC_PIPE_MODES
     if (a.trace) {

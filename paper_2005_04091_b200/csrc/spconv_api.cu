@@ -174,11 +174,18 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         // (gen_dispatch2.py), two per 16-byte stream word.
         // Ascending case within a channel, channels in order: every output row's
         // taps are consumed in ascending colidx order (the FP32 contract).
-        p->gpc = std::min(p->num_groups, 8);
+        // warps (= groups) per CTA: 8 at R = 4; at R = 2 up to 12, spread evenly over
+        // the group sets (32 groups -> 3 sets of 11 warps, not 12 + 12 + 8)
+        if (R == 2) {
+            const int sets = (p->num_groups + 11) / 12;
+            p->gpc = (p->num_groups + sets - 1) / sets;
+        } else {
+            p->gpc = std::min(p->num_groups, 8);
+        }
         // brx.idx threaded code (default; measured faster on B200) or the tap-mask walk
         p->pipe_dispatch = 0;
         if (const char *e = std::getenv("SPCONV_PIPE_DISPATCH"))
-            if (std::strcmp(e, "mask") == 0) p->pipe_dispatch = 1;
+            if (std::strcmp(e, "mask") == 0 && R == 4) p->pipe_dispatch = 1;
         p->num_gsets = (p->num_groups + p->gpc - 1) / p->gpc;
         const int hdr = ((p->gpc * 4 + 15) / 16) * 16;
         std::vector<uint4> out;
@@ -442,9 +449,13 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
     else
         p->kernel = o.kernel;
     int R = o.rows_per_group;
-    if (R == 0)
+    if (R == 0) {
         R = p->kernel == SPCONV_KERNEL_PIPE ? 4 : spconv::tiled_default_R(C, F, double(nnz) / (double(F) * ncol));
-    if ((p->kernel == SPCONV_KERNEL_PIPE && R != 4) ||
+        // A/B switch for the pipe kernel's rows per group
+        if (p->kernel == SPCONV_KERNEL_PIPE)
+            if (const char *e = std::getenv("SPCONV_PIPE_R")) R = std::atoi(e);
+    }
+    if ((p->kernel == SPCONV_KERNEL_PIPE && R != 4 && R != 2) ||
         (p->kernel == SPCONV_KERNEL_TILED && R != 4 && R != 8)) {
         delete p;
         return SPCONV_ERR_UNSUPPORTED;

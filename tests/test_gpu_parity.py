@@ -595,6 +595,38 @@ def test_pipe_tuning_options_keep_the_bits(env, monkeypatch):
     _check_full(synthgen.CONFIGS["c3"], "pipe", True, N=2)
 
 
+@pytest.mark.parametrize("name,fused,N", [("c1", False, 1), ("c2", False, 2), ("c3", True, 2), ("c2", False, 19),
+                                          ("c4_50", False, 3), ("c4_95", False, 76), ("c5", False, 1)])
+def test_pipe_two_rows_per_group(name, fused, N, monkeypatch):
+    """Pipelined kernel with R = 2 rows per group (11-12 warps per CTA instead of 8,
+    group sets spread evenly; SPCONV_PIPE_R=2): only the grouping changes, every output
+    row is still one ascending fma chain -- bits equal to the oracle, stream-K included
+    (c2 N=19, c4_95 N=76)."""
+    monkeypatch.setenv("SPCONV_PIPE_R", "2")
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N)
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=1, integer=True)
+
+
+def test_pipe_two_rows_per_group_epilogues_and_plan_info():
+    """R = 2 through the explicit option (rows_per_group=2): plan info, and the fused
+    ReLU + residual epilogue in place -- bits equal to the oracle."""
+    from paper_2005_04091_b200 import SparseConv2d
+    cfg = synthgen.CONFIGS["c2"].with_batch(2)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, cfg.K, cfg.stride, cfg.pad, c.rowptr, c.colidx, c.values,
+                         b, device=0, kernel="pipe", rows_per_group=2)
+    assert layer.info["rows_per_group"] == 2 and layer.info["num_groups"] == 32
+    x = torch.from_numpy(L.x).cuda()
+    r = synthgen.make_input((2, cfg.F, layer.Ho, layer.Wo), 4243)
+    ref = oracle.conv_ex_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, residual=r, relu=True)
+    yt = torch.from_numpy(r).cuda()
+    layer.forward_ex(x, relu=True, residual=yt, out=yt)
+    assert np.array_equal(bits(yt.cpu().numpy()), bits(ref))
+    layer.close()
+
+
 def test_forward_host_chunk_counts(monkeypatch):
     """spconv_forward_host with 1, 5 and 16 pipelined chunks: the same bits."""
     cfg = synthgen.CONFIGS["c2"].with_batch(7)
