@@ -451,6 +451,11 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
     int R = o.rows_per_group;
     if (R == 0) {
         R = p->kernel == SPCONV_KERNEL_PIPE ? 4 : spconv::tiled_default_R(C, F, double(nnz) / (double(F) * ncol));
+        // pipe: R = 2 (12 warps) once a row has >= 3.5 nonzeros per input channel
+        // (density >= ~0.39): the per-channel window reload is then amortised and the
+        // extra warps hide more dispatch latency.  Measured crossover 3.2-3.6 on the c2,
+        // c4 and c5 shapes (profiles/r01_r_sweep.jsonl)
+        if (p->kernel == SPCONV_KERNEL_PIPE && double(nnz) >= 3.5 * double(F) * double(C)) R = 2;
         // A/B switch for the pipe kernel's rows per group
         if (p->kernel == SPCONV_KERNEL_PIPE)
             if (const char *e = std::getenv("SPCONV_PIPE_R")) R = std::atoi(e);

@@ -16,10 +16,12 @@ for c in c1 c2 c3 c4_50 c4_80 c4_90 c4_95 c5; do
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 200 --csv \
    --log-file gpurun_out/launches_c2.csv python bench.py --steps 300 --warmup 20 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
-for c in c2 c3 c4_80 c5; do
+for c in c2 c3 c4_50 c4_80 c5; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:pipe_kernel -s 3 -c 1 \
      -o gpurun_out/full_$c -f python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/full_$c.log 2>&1
 done
+timeout 600 python scripts/breakeven.py --shape c2 > gpurun_out/breakeven_c2.jsonl 2> gpurun_out/breakeven_c2.err
+timeout 600 python scripts/breakeven.py --shape c4 > gpurun_out/breakeven_c4.jsonl 2> gpurun_out/breakeven_c4.err
 timeout 600 python scripts/lstm_bench.py --batch 64 --reps 10 > gpurun_out/lstm_b64.jsonl 2>&1
 timeout 600 python scripts/lstm_bench.py --batch 1 --reps 10 > gpurun_out/lstm_b1.jsonl 2>&1
 for tool in memcheck synccheck; do

@@ -50,6 +50,13 @@ def main():
     print("c2 pipe cp.async", "ok" if ok else "MISMATCH")
     good &= ok
     del os.environ["SPCONV_PIPE_STAGING"]
+    # R = 2 rows per group (11-12 warps per CTA), incl. ordered stream-K (c2 N=19)
+    os.environ["SPCONV_PIPE_R"] = "2"
+    for name, N in (("c2", 2), ("c2", 19), ("c4_50", 2)):
+        ok = check(synthgen.CONFIGS[name].with_batch(N), "pipe")
+        print(name, N, "pipe R=2", "ok" if ok else "MISMATCH", flush=True)
+        good &= ok
+    del os.environ["SPCONV_PIPE_R"]
     from paper_2005_04091_b200.lstm import SEQUENTIAL, WAVEFRONT, SparseLSTM
     layers, xl = synthgen.make_lstm(2, 24, 16, 0.3, 4, 3)
     net = SparseLSTM(24, 16, layers)

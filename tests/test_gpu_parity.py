@@ -627,6 +627,20 @@ def test_pipe_two_rows_per_group_epilogues_and_plan_info():
     layer.close()
 
 
+@pytest.mark.parametrize("name,density,want_R", [("c2", 0.2, 4), ("c2", 0.3, 4), ("c2", 0.5, 2),
+                                                 ("c4_50", 0.5, 2), ("c4_50", 1.0, 2)])
+def test_pipe_auto_rows_per_group(name, density, want_R, monkeypatch):
+    """AUTO picks R = 2 once rows hold >= 3.5 nonzeros per input channel (the measured
+    crossover, profiles/r01_r_sweep.jsonl) and R = 4 below; bits equal to the oracle."""
+    monkeypatch.delenv("SPCONV_PIPE_R", raising=False)
+    cfg = synthgen.CONFIGS[name].with_density(density).with_batch(2)
+    L = synthgen.make_layer(cfg)
+    layer = _layer(cfg, L.csr, _bias(cfg), "auto")
+    assert layer.info["rows_per_group"] == want_R
+    layer.close()
+    _check_full(cfg, "auto", False)
+
+
 def test_forward_host_chunk_counts(monkeypatch):
     """spconv_forward_host with 1, 5 and 16 pipelined chunks: the same bits."""
     cfg = synthgen.CONFIGS["c2"].with_batch(7)
