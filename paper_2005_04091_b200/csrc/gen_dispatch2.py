@@ -24,8 +24,9 @@ FMA operand register (its latency hides under the branch).  Long case bodies (T*
 what hide the jump latency (scripts/probes/dispatch_probe.cu measures it).
 
 One walk covers all channels of a pipeline stage: case R*9 ("next channel")
-advances the window pointer by one staged channel and reloads the window
-from shared memory, case R*9+1 ends the walk.
+advances the window pointer by k staged channels (k = the marker entry's value
+field: channels without nonzeros for the group are skipped, not reloaded) and
+reloads the window from shared memory, case R*9+1 ends the walk.
 
 Run: python gen_dispatch2.py [out]  (build.py runs it when the output is stale).
 """
@@ -116,7 +117,10 @@ def gen(R: int, T: int, S: int) -> str:
     # next channel: advance the window and reload it (T+2 rows of PAIRS pairs)
     L.append(f"$D{tag}_{ncase}:")
     L += head()
-    L.append(f"add.u32 {WP}, {WP}, {CHS};")
+    # the marker's value field holds k >= 1, the channels to advance (runs of channels
+    # without nonzeros for this group are skipped in one step)
+    L.append("mov.b32 %%wa, %%vf;")
+    L.append(f"mad.lo.u32 {WP}, %%wa, {CHS}, {WP};")
     L.append(f"mov.b32 %%wa, {WP};")
     for i in range(T + 2):
         j = 0

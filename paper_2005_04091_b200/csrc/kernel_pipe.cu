@@ -190,17 +190,33 @@ __device__ __forceinline__ void mask_walk(uint64_t (&acc)[R][PT][PS / 2], const 
 // marker entry (index + 1) is a valid lead entry for a walk starting at channel k.
 // Warp-cooperative (ballot over 32 entries at a time); the caller asks for k < the
 // stage's channel count, so the marker exists.
-__device__ __forceinline__ int find_marker(const uint2 *seg, int k, int lane, uint32_t marker) {
-    int seen = 0;
+// brx.idx streams: markers (entry j + 1 when seg[j].y == marker) advance the window by
+// k channels (k = the marker entry's value field).  Returns the j of the first marker
+// whose target channel (running sum of the advances) is >= cl, with *target set, or
+// the j whose .y is the end case (marker + 1) when no later marker reaches cl
+// (*target = -1).  Warp-collective.
+__device__ __forceinline__ int find_channel(const uint2 *seg, int cl, int lane, uint32_t marker, int *target) {
+    int run = 0;
     for (int base = 0;; base += 32) {
-        const unsigned m = __ballot_sync(0xffffffffu, seg[base + lane].y == marker);
-        const int c = __popc(m);
-        if (seen + c >= k) {
-            unsigned mm = m;
-            for (int i = 1; i < k - seen; ++i) mm &= mm - 1;
-            return base + __ffs(mm) - 1;
+        const uint2 e = seg[base + lane];
+        const bool mk = e.y == marker, en = e.y == marker + 1u;
+        uint32_t nx = __shfl_down_sync(0xffffffffu, e.x, 1);
+        if (lane == 31 && mk) nx = seg[base + 32].x;
+        int sc = mk ? int(nx) : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, sc, o);
+            if (lane >= o) sc += t;
         }
-        seen += c;
+        const unsigned m = __ballot_sync(0xffffffffu, (mk && run + sc >= cl) || en);
+        if (m) {
+            const int l = __ffs(m) - 1;
+            const int t = __shfl_sync(0xffffffffu, run + sc, l);
+            const bool isend = __shfl_sync(0xffffffffu, en ? 1 : 0, l) != 0;
+            *target = isend ? -1 : t;
+            return base + l;
+        }
+        run += __shfl_sync(0xffffffffu, sc, 31);
     }
 }
 
@@ -320,7 +336,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     // chunks [0, hA)], nf whole units, [tail of unit ut: channels [tcs, C), chunks
     // [tc0, nch)].  Stream-K ranges are counted in input channels, so a split can fall
     // inside a stage: the head walks only the first channels of its last stage, the
-    // tail starts its first stage part-way (find_marker).
+    // tail starts its first stage part-way (find_channel).
     // The schedule lives in shared memory and is re-read where needed: values kept
     // in registers across the dispatcher's asm would cost it registers (measured: one
     // extra MOV on every case's jump-target path, -4% on c5).
@@ -477,18 +493,26 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
                 if (cl0 > 0 || cl1 < ncl) { // warp-uniform, at most twice per CTA
                     uint2 *seg = reinterpret_cast<uint2 *>(smem + size_t(s) * stage_bytes + a.in_pad + seg_off);
                     if (cl1 < ncl) {
-                        // end the walk after channel cl1 - 1: its marker becomes "end" (this
-                        // warp's private copy of the segment; the refill overwrites it)
-                        const int j = find_marker(seg, cl1, lane, 9u * R);
-                        if (lane == 0) seg[j].y = 9u * R + 1u;
+                        // end the walk before channel cl1: the first marker reaching it becomes
+                        // "end" (this warp's private copy of the segment; the refill overwrites it)
+                        int t;
+                        const int j = find_channel(seg, cl1, lane, 9u * R, &t);
+                        if (lane == 0 && t >= 0) seg[j].y = 9u * R + 1u;
                         __syncwarp();
                     }
                     if (cl0 > 0) {
-                        // start at channel cl0: the marker entry before it is the lead entry
-                        const int j = find_marker(seg, cl0, lane, 9u * R);
-                        sp += uint32_t(j + 1) * 8u;
-                        wp += uint32_t(cl0) * ch_bytes;
-                        wptr += size_t(cl0) * ch_bytes;
+                        // start at channel cl0: the first marker reaching it is the lead entry
+                        // and the window starts at its target (channels cl0..t-1 hold no
+                        // nonzeros of this group); none -> start at the end entry
+                        int t;
+                        const int j = find_channel(seg, cl0, lane, 9u * R, &t);
+                        if (t >= 0) {
+                            sp += uint32_t(j + 1) * 8u;
+                            wp += uint32_t(t) * ch_bytes;
+                            wptr += size_t(t) * ch_bytes;
+                        } else {
+                            sp += uint32_t(j) * 8u;
+                        }
                     }
                 }
 #pragma unroll

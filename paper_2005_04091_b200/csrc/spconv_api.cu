@@ -271,9 +271,15 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                         // the walk order (case, value) of this warp's stage, then stored with
                         // each entry carrying the NEXT entry's case behind a lead entry, so the
                         // case id of k+2 is loaded while case k+1 is dispatched
+                        // A "next channel" marker carries k (>= 1) in its value field: the walk
+                        // skips channels without nonzeros for this group instead of reloading
+                        // the window for each (the window starts at channel c0).
                         std::vector<std::pair<uint32_t, uint32_t>> walk;
+                        int at = c0;
                         for (int c = c0; c < c1; ++c) {
-                            if (g < p->num_groups) {
+                            if (g < p->num_groups && !byc[size_t(g)][size_t(c)].empty()) {
+                                if (c > at) walk.push_back({NEXT, uint32_t(c - at)});
+                                at = c;
                                 auto v = byc[size_t(g)][size_t(c)];
                                 std::stable_sort(v.begin(), v.end(),
                                                  [](const std::pair<int, float> &a, const std::pair<int, float> &b) {
@@ -285,8 +291,8 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                                     walk.push_back({uint32_t(e.first), bits});
                                 }
                             }
-                            walk.push_back({c + 1 < c1 ? NEXT : END, 0u});
                         }
+                        walk.push_back({END, 0u});
                         // 8-byte entries {value, case of the next entry} behind a lead entry
                         // {0, first case}, two per 16-byte stream word (a segment is padded
                         // to a whole word)
