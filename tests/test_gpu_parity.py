@@ -641,6 +641,36 @@ def test_pipe_auto_rows_per_group(name, density, want_R, monkeypatch):
     _check_full(cfg, "auto", False)
 
 
+@pytest.mark.parametrize("keep,sk", [(5, "1"), (7, "1"), (3, "0"), (64, "1")])
+@pytest.mark.parametrize("R", ["4", "2"])
+def test_pipe_skipped_channels_with_stream_k_splits(keep, sk, R, monkeypatch):
+    """Rows with nonzeros only in every keep-th input channel (long runs of channels
+    with no nonzero for a group, which the walk skips in one step), with ordered
+    stream-K (c2 shape, N=19: splits land at arbitrary channels, also inside skipped
+    runs) and without, at R = 4 and R = 2 -- bits equal to the oracle."""
+    monkeypatch.setenv("SPCONV_PIPE_SK", sk)
+    monkeypatch.setenv("SPCONV_PIPE_R", R)
+    cfg = synthgen.CONFIGS["c2"].with_batch(19)
+    L = synthgen.make_layer(cfg.with_density(0.5))
+    c = L.csr
+    rows, cols, vals = [0], [], []
+    for f in range(cfg.F):
+        for j in range(c.rowptr[f], c.rowptr[f + 1]):
+            ch = int(c.colidx[j]) // 9
+            if (ch + f) % keep == 0:  # a different channel phase per row
+                cols.append(int(c.colidx[j]))
+                vals.append(float(c.values[j]))
+        rows.append(len(cols))
+    csr = synthgen.CSR(cfg.F, cfg.C, 3, np.array(rows, np.int32), np.array(cols, np.int32),
+                       np.array(vals, np.float32))
+    b = _bias(cfg)
+    layer = _layer(cfg, csr, b, "pipe")
+    y = layer(torch.from_numpy(L.x).cuda()).cpu().numpy()
+    ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b)
+    assert np.array_equal(bits(y), bits(ref))
+    layer.close()
+
+
 def test_forward_host_chunk_counts(monkeypatch):
     """spconv_forward_host with 1, 5 and 16 pipelined chunks: the same bits."""
     cfg = synthgen.CONFIGS["c2"].with_batch(7)
