@@ -66,15 +66,23 @@ enum {
     SPCONV_ERR_ALIAS = -9        /* y (or argmax) overlaps x                        */
 };
 
-/* Kernel selection (spconv_create_ex).  AUTO picks the pipelined kernel when
- * the shape is supported by it (K = 3, stride 1, pad 1, Wo <= 125), else the
- * register-tiled v1 kernel (K = 3, stride 1, pad 1), else the generic kernel.
+/* Kernel selection (spconv_create_ex).  AUTO picks the dense kernel for K = 3,
+ * stride 1, pad 1 layers at or above the break-even density, else the pipelined
+ * kernel when the shape is supported by it (K = 3, stride 1, pad 1, Wo <= 125),
+ * else the register-tiled v1 kernel when its staging fits shared memory, else the
+ * generic kernel.
  * All are CUDA kernels; all obey the same arithmetic contract. */
 enum {
     SPCONV_KERNEL_AUTO = 0,
     SPCONV_KERNEL_GENERIC = 1,   /* one thread per output; any supported shape    */
     SPCONV_KERNEL_TILED = 2,     /* v1: row-grouped register tiles, cp.async      */
-    SPCONV_KERNEL_PIPE = 3       /* v2: warp-specialised TMA pipeline, FFMA2      */
+    SPCONV_KERNEL_PIPE = 3,      /* v2: warp-specialised TMA pipeline, FFMA2      */
+    SPCONV_KERNEL_DENSE = 4      /* dense FP32 direct conv of the densified filters
+                                    (conv-only calls; fused / epilogue calls use PIPE).
+                                    Bitwise equal to the others: a zero tap is an
+                                    exact no-op of the FP32 contract.  AUTO picks it
+                                    for layers denser than the measured break-even
+                                    (DESIGN.md NEXT-1) */
 };
 
 typedef struct spconv_plan_s *spconv_plan_t;
@@ -89,7 +97,7 @@ typedef struct {
     int C, H, W, F, K, stride, pad, Ho, Wo;
     int64_t nnz;
     int device;
-    int kernel;           /* kernel the plan will launch (GENERIC or TILED)      */
+    int kernel;           /* kernel a conv-only call launches (SPCONV_KERNEL_*)  */
     int rows_per_group;   /* tiled: R                                            */
     int num_groups;       /* tiled: ceil(F / R)                                  */
     int64_t device_bytes; /* device memory held by the plan                      */
@@ -172,6 +180,26 @@ int spconv_destroy(spconv_plan_t plan);
 int spconv_output_dims(spconv_plan_t plan, int N, int fused, int64_t dims[4]);
 
 int spconv_plan_info(spconv_plan_t plan, spconv_plan_info_t *info);
+
+/* The launch schedule of one forward of N images (fused != 0: the fused block)
+ * with input x (its alignment selects the staging path; NULL = 16-byte aligned).
+ * Describes exactly what spconv_forward / spconv_fused_relu_maxpool would launch
+ * (same decision code); the parity tests assert on it (stream-K really engaged,
+ * band units, staging path).  The pipe-only fields are 0 for other kernels. */
+typedef struct {
+    int kernel;             /* SPCONV_KERNEL_* the call launches                   */
+    int rows_per_group;     /* output channels per register tile                  */
+    int grid;               /* pipe: persistent CTAs (<= SM count)                */
+    int stream_k;           /* pipe: 1 = ordered stream-K split of the units      */
+    int64_t units;          /* pipe: (pixel block, group set) work units          */
+    int band;               /* pipe: 1 = units are one-tile-row bands             */
+    int staging;            /* pipe: 0 TMA on x, 1 TMA on a padded copy, 2 cp.async */
+    int channels_per_stage; /* pipe: input channels per pipeline stage            */
+    int stages;             /* pipe: pipeline depth (shared-memory ring)          */
+    int launches;           /* kernel launches per call                           */
+    int reserved[7];
+} spconv_launch_info_t;
+int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spconv_launch_info_t *info);
 
 /* Static string for a status code (never NULL). */
 const char *spconv_status_string(int status);

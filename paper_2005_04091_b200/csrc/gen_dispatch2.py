@@ -36,6 +36,12 @@ import sys
 # (R, T, S) variants instantiated by kernel_pipe.cu
 VARIANTS = [(4, 4, 8), (4, 8, 4), (4, 4, 4), (2, 8, 4)]
 MASK_VARIANTS = [(4, 8, 4)]
+# dispatcher code variants (A/B via -DSPC_DISPATCH_VARIANT=v): 0 = round-1 walk,
+# 1 = sp advanced in the case head (no write-after-read stall at the case end),
+# 2 = 1 + a single brx.idx site (one jump table instead of one per case),
+# 3 = 1 + the new sp forced before the loads, 4 = 3 + a single site,
+# 5 = 3 + the next case id loaded (volatile) at the top of the case
+DISPATCH_VARIANTS = [0, 1, 2, 3, 4, 5]
 # Stream entries are 8 bytes {value (f32), case of the NEXT entry (u32)}: the value
 # is loaded straight into the FMA operand at the end of a case (FFMA2 takes it as a
 # broadcast .F32 operand), the next case id early -- no register copies.  (Measured
@@ -44,7 +50,7 @@ MASK_VARIANTS = [(4, 8, 4)]
 ENT = 8
 
 
-def gen(R: int, T: int, S: int) -> str:
+def gen(R: int, T: int, S: int, variant: int = 0) -> str:
     PAIRS = (S + 2) // 2  # window pairs per row
     SH = S // 2           # accumulator pairs per output row
     nacc = R * T * SH
@@ -59,21 +65,50 @@ def gen(R: int, T: int, S: int) -> str:
 
     def head():
         # case id of entry k+1 (it came with entry k): its jump-table load overlaps
-        # this case's FMAs
-        return ["mov.b32 %%cn, %%cx;"]
+        # this case's FMAs.  variant >= 1: sp advances here, one branch away from the
+        # last load that read it (advancing it after that load stalled the end of
+        # every case on the load's register read, a write-after-read hazard)
+        out = ["mov.b32 %%cn, %%cx;"]
+        if variant >= 1:
+            # the stride comes in a register (SPC2_ENT_REG): with an immediate, ptxas
+            # folds the add into the loads' offsets and copies the new sp back after
+            # the last load -- the very hazard this avoids
+            out.append(f"add.u32 %%sp, %%sp, {ENTR};")
+            if variant >= 3:
+                # a no-op mask (entries are 8-byte aligned) that ptxas cannot fold into
+                # the loads' address: the new sp must exist before them
+                out.append("and.b32 %%sp, %%sp, -8;")
+            if variant >= 5:
+                # the case id of entry k+2 at the top (volatile: not merged with the
+                # value load at the end into one 64-bit load, which would put the
+                # load's latency in front of the next case's jump-table load)
+                out.append("ld.volatile.shared.u32 %%cx, [%%sp+4];")
+        return out
 
     def tail():
         # after the FMAs, entry k+1 = {v, case of k+2}: the value lands straight in
         # the operand register; sp -> entry k+2
-        return ["ld.shared.f32 %%vf, [%%sp];",
-                "ld.shared.u32 %%cx, [%%sp+4];",
-                f"add.u32 %%sp, %%sp, {ENT};",
-                f"brx.idx.uni %%cn, $D{tag}_T;"]
+        if variant >= 5:
+            out = ["ld.shared.f32 %%vf, [%%sp];"]
+        elif variant >= 1:
+            out = ["ld.shared.f32 %%vf, [%%sp];",
+                   "ld.shared.u32 %%cx, [%%sp+4];"]
+        else:
+            out = ["ld.shared.f32 %%vf, [%%sp];",
+                   "ld.shared.u32 %%cx, [%%sp+4];",
+                   f"add.u32 %%sp, %%sp, {ENT};"]
+        if variant in (2, 4):
+            # one dispatch site: a single jump table stays in the constant cache
+            out.append(f"bra.uni $D{tag}_X;")
+        else:
+            out.append(f"brx.idx.uni %%cn, $D{tag}_T;")
+        return out
 
     P = f"%{nacc}"  # u32 shared-memory stream address, in/out
     WP = f"%{nacc + 1 + (T + 2) * PAIRS}"  # u32 window address (in/out)
     CHS = f"%{nacc + 2 + (T + 2) * PAIRS}"  # channel stride in bytes (in)
     ROWB = f"%{nacc + 3 + (T + 2) * PAIRS}"  # row stride in bytes (in)
+    ENTR = f"%{nacc + 4 + (T + 2) * PAIRS}"  # entry stride in bytes (in; == ENT)
     ncase = R * 9
     tag = f"R{R}T{T}S{S}"
     L = []
@@ -89,8 +124,12 @@ def gen(R: int, T: int, S: int) -> str:
     L.append("ld.shared.u32 %%cn, [%%sp+4];")
     L.append(f"ld.shared.f32 %%vf, [%%sp+{ENT}];")
     L.append(f"ld.shared.u32 %%cx, [%%sp+{ENT + 4}];")
-    L.append(f"add.u32 %%sp, %%sp, {2 * ENT};")
+    # variant 0: sp -> entry k+1 on entry to case k; variant >= 1: sp -> entry k
+    # (the case head advances it)
+    L.append(f"add.u32 %%sp, %%sp, {2 * ENT if variant == 0 else ENT};")
     L.append(f"$D{tag}_T: .branchtargets " + ", ".join(f"$D{tag}_{i}" for i in range(ncase + 2)) + ";")
+    if variant in (2, 4):
+        L.append(f"$D{tag}_X:")
     L.append(f"brx.idx.uni %%cn, $D{tag}_T;")
     for i in range(ncase):
         # tap-major case numbering: case = (ky*3 + kx)*R + r
@@ -133,6 +172,8 @@ def gen(R: int, T: int, S: int) -> str:
             L.append(f"add.u32 %%wa, %%wa, {ROWB};")
     L += tail()
     L.append(f"$D{tag}_{ncase + 1}:")
+    if variant >= 1:
+        L.append(f"add.u32 %%sp, %%sp, {ENTR};")
     L.append(f"mov.b32 {P}, %%sp;")
     L.append("}")
     asm = "\\n\\t".join(L)
@@ -141,7 +182,7 @@ def gen(R: int, T: int, S: int) -> str:
     return (f"#define SPC2_DISPATCH_{tag}(acc, xw, sp, wp, chs, rowb) \\\n"
             f"    asm volatile(\"{asm}\" \\\n"
             f"                 : {outs}, \"+r\"(sp), {xws}, \"+r\"(wp) \\\n"
-            f"                 : \"r\"(chs), \"r\"(rowb) \\\n"
+            f"                 : \"r\"(chs), \"r\"(rowb), \"r\"(SPC2_ENT_REG) \\\n"
             f"                 : \"memory\")\n")
 
 
@@ -250,9 +291,15 @@ def gen_mask(R: int, T: int, S: int) -> str:
 
 def main(out_path: str) -> None:
     text = ["// GENERATED by gen_dispatch2.py — do not edit.\n"]
-    for R, T, S in VARIANTS:
-        text.append(f"// R={R} rows, thread tile T={T} x S={S}, window {T + 2} x {S + 2} as 64-bit pairs.\n")
-        text.append(gen(R, T, S))
+    text.append("#ifndef SPC_DISPATCH_VARIANT\n#define SPC_DISPATCH_VARIANT 3\n#endif\n")
+    text.append(f"// the stream entry stride ({ENT}) as a register the compiler cannot fold\n"
+                f"#ifndef SPC2_ENT_REG\n#define SPC2_ENT_REG {ENT}u\n#endif\n")
+    for v in DISPATCH_VARIANTS:
+        text.append(f"#if SPC_DISPATCH_VARIANT == {v}\n")
+        for R, T, S in VARIANTS:
+            text.append(f"// R={R} rows, thread tile T={T} x S={S}, window {T + 2} x {S + 2} as 64-bit pairs.\n")
+            text.append(gen(R, T, S, v))
+        text.append("#endif\n")
     for R, T, S in MASK_VARIANTS:
         text.append(f"// mask walk: R={R} rows, thread tile T={T} x S={S}.\n")
         text.append(gen_mask(R, T, S))

@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "async_copy.cuh"
 #include "spconv_internal.h"
 
 namespace spconv {
@@ -65,6 +66,7 @@ struct PipeArgs {
     int band; // 1: the ipb slots of a unit are tile-row bands of the flattened (image, tile row) sequence
     int gpc, num_groups, num_gsets;
     int tma;
+    int ent; // == 8, the tap-stream entry stride: a runtime value so ptxas cannot fold it (SPC2_ENT_REG)
     // ordered stream-K (sk = 1): CTA b owns the contiguous chunk range
     // [b*U*nch/grid, (b+1)*U*nch/grid) of the U units; a unit cut by a range end is
     // started by CTA b (its "head", done FIRST, accumulators parked in sk_part slot b)
@@ -73,66 +75,19 @@ struct PipeArgs {
     int sk;
     ulonglong2 *sk_part;              // [grid][gpc][R*PT*PS/4][32 lanes]
     unsigned long long *sk_flag;      // [grid][gpc]: == epoch when slot (b, warp) is ready
+    unsigned *sk_ticket;              // [2]: arrival ticket, finished CTAs (0 between launches)
     unsigned long long epoch;
     unsigned long long *trace; // debug (SPCONV_PIPE_TRACE): per CTA 8 timestamps, or null
     int rev;                   // debug (SPCONV_PIPE_REV=1): CTA b does the work of CTA grid-1-b
+    unsigned long long *prof;  // diagnostic builds (-DSPC_PROF): per-phase clock sums, or null
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void tma_load_4d(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0,
-                                            int c1, int c2, int c3) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void cp_async_4(uint32_t dst, const void *src, bool valid) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
+using namespace dev; // mbarrier / TMA / bulk-copy wrappers (async_copy.cuh)
 
 __device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float(uint32_t(v)); }
 __device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(uint32_t(v >> 32)); }
 
+#define SPC2_ENT_REG (a.ent)
 #include "dispatch2_gen.inc"
 
 // Mask dispatcher (SPCONV_PIPE_DISPATCH=mask; the brx.idx walk is the default,
@@ -195,13 +150,16 @@ __device__ __forceinline__ void mask_walk(uint64_t (&acc)[R][PT][PS / 2], const 
 // whose target channel (running sum of the advances) is >= cl, with *target set, or
 // the j whose .y is the end case (marker + 1) when no later marker reaches cl
 // (*target = -1).  Warp-collective.
-__device__ __forceinline__ int find_channel(const uint2 *seg, int cl, int lane, uint32_t marker, int *target) {
+// Reads only the warp's own segment (nent entries): never past the stage's stream
+// chunk, never another warp's segment (which that warp may be patching).
+__device__ __forceinline__ int find_channel(const uint2 *seg, int nent, int cl, int lane, uint32_t marker,
+                                            int *target) {
     int run = 0;
     for (int base = 0;; base += 32) {
-        const uint2 e = seg[base + lane];
+        const uint2 e = base + lane < nent ? seg[base + lane] : make_uint2(0u, 0u);
         const bool mk = e.y == marker, en = e.y == marker + 1u;
         uint32_t nx = __shfl_down_sync(0xffffffffu, e.x, 1);
-        if (lane == 31 && mk) nx = seg[base + 32].x;
+        if (lane == 31 && mk) nx = base + 32 < nent ? seg[base + 32].x : 0u;
         int sc = mk ? int(nx) : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -308,7 +266,25 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    const int bid = a.rev ? int(gridDim.x) - 1 - int(blockIdx.x) : int(blockIdx.x); // work index
+#ifdef SPC_PROF
+    // diagnostic: clock cycles per phase, summed over warps: [0] other (prologue, loop
+    // overhead), [1] waiting for a stage, [2] the tap walk, [3] stage release and refill,
+    // [4] park / epilogue and the next unit's setup
+    __shared__ unsigned long long s_prof[5];
+    if (threadIdx.x < 5) s_prof[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned prof_t = (unsigned)clock();
+    int prof_ph = 0;
+#define SPC_PROF_MARK(next)                                                    \
+    do {                                                                      \
+        const unsigned t_ = (unsigned)clock();                                \
+        if (lane == 0) atomicAdd(&s_prof[prof_ph], (unsigned long long)(t_ - prof_t)); \
+        prof_t = t_;                                                          \
+        prof_ph = (next);                                                     \
+    } while (0)
+#else
+#define SPC_PROF_MARK(next) do { } while (0)
+#endif
     const int ns = a.nstage;
     unsigned long long *tr = a.trace ? a.trace + size_t(blockIdx.x) * 8 : nullptr;
     if (tr && threadIdx.x == 0) {
@@ -340,31 +316,6 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     // The schedule lives in shared memory and is re-read where needed: values kept
     // in registers across the dispatcher's asm would cost it registers (measured: one
     // extra MOV on every case's jump-target path, -4% on c5).
-    struct Sched {
-        int hA, uh, tc0, tC, ut, nf, uf0, hc, tcs, total;
-    };
-    __shared__ Sched sch;
-    if (threadIdx.x == 0) {
-        Sched q{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-        if (a.sk) {
-            const int C = a.C;
-            const int64_t tot = int64_t(nunits) * C;
-            const int64_t s0 = tot * bid / gridDim.x, e0 = tot * (bid + 1) / gridDim.x;
-            if (e0 % C) { q.hc = int(e0 % C); q.uh = int(e0 / C); q.hA = (q.hc + a.cc - 1) / a.cc; }
-            if (s0 % C) { q.tcs = int(s0 % C); q.ut = int(s0 / C); q.tc0 = q.tcs / a.cc; q.tC = nch - q.tc0; }
-            q.uf0 = int((s0 + C - 1) / C);
-            q.nf = int(e0 / C) - q.uf0;
-        } else {
-            q.uf0 = bid;
-            q.nf = bid < nunits ? (nunits - 1 - bid) / int(gridDim.x) + 1 : 0;
-        }
-        q.total = q.hA + q.nf * nch + q.tC;
-        sch = q;
-    }
-    __syncthreads();
-    const int &hA = sch.hA, &uh = sch.uh, &tc0 = sch.tc0, &tC = sch.tC, &ut = sch.ut, &nf = sch.nf,
-              &uf0 = sch.uf0, &hc = sch.hc, &tcs = sch.tcs, &total = sch.total;
-    auto full_unit = [&](int j) { return a.sk ? uf0 + j : uf0 + j * int(gridDim.x); };
 
     for (int i = threadIdx.x; i < ncs; i += blockDim.x) s_cstart[i] = __ldg(a.chunk_start + i);
     for (int i = threadIdx.x; i < a.num_groups * R; i += blockDim.x) s_rows[i] = __ldg(a.group_rows + i);
@@ -385,6 +336,41 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     // were read above.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    struct Sched {
+        int hA, uh, tc0, tC, ut, nf, uf0, hc, tcs, total;
+    };
+    __shared__ Sched sch;
+    __shared__ int s_bid;
+    if (threadIdx.x == 0) {
+        // work index.  Stream-K: an arrival ticket (taken after griddepcontrol.wait, so
+        // the previous launch on this workspace has finished and reset the counter):
+        // CTA b's tail waits only for the head of ticket b-1, whose CTA is already
+        // running, so the wait cannot depend on a CTA that is not resident (forward
+        // progress under MPS, green contexts or concurrent kernels).
+        const int t = a.sk ? int(atomicAdd(a.sk_ticket, 1u)) : int(blockIdx.x);
+        const int bid = a.rev ? int(gridDim.x) - 1 - t : t;
+        s_bid = bid;
+        Sched q{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (a.sk) {
+            const int C = a.C;
+            const int64_t tot = int64_t(nunits) * C;
+            const int64_t s0 = tot * bid / gridDim.x, e0 = tot * (bid + 1) / gridDim.x;
+            if (e0 % C) { q.hc = int(e0 % C); q.uh = int(e0 / C); q.hA = (q.hc + a.cc - 1) / a.cc; }
+            if (s0 % C) { q.tcs = int(s0 % C); q.ut = int(s0 / C); q.tc0 = q.tcs / a.cc; q.tC = nch - q.tc0; }
+            q.uf0 = int((s0 + C - 1) / C);
+            q.nf = int(e0 / C) - q.uf0;
+        } else {
+            q.uf0 = bid;
+            q.nf = bid < nunits ? (nunits - 1 - bid) / int(gridDim.x) + 1 : 0;
+        }
+        q.total = q.hA + q.nf * nch + q.tC;
+        sch = q;
+    }
+    __syncthreads();
+    const int bid = s_bid;
+    const int &hA = sch.hA, &uh = sch.uh, &tc0 = sch.tc0, &tC = sch.tC, &ut = sch.ut, &nf = sch.nf,
+              &uf0 = sch.uf0, &hc = sch.hc, &tcs = sch.tcs, &total = sch.total;
+    auto full_unit = [&](int j) { return a.sk ? uf0 + j : uf0 + j * int(gridDim.x); };
 
     auto fill = [&](int kk, int s) {
         int u, ch;
@@ -472,7 +458,9 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         }
 
         for (int ch = c0; ch < c1; ++ch) {
+            SPC_PROF_MARK(1);
             mbar_wait(smem_u32(&full_bar[s]), rnd & 1);
+            SPC_PROF_MARK(2);
             if (active) {
                 const unsigned char *stage = smem + size_t(s) * stage_bytes;
                 const uint32_t st_base = smem0 + uint32_t(s) * stage_bytes + uint32_t(a.in_pad);
@@ -492,11 +480,17 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
                 const unsigned char *wptr = stage + win_off;
                 if (cl0 > 0 || cl1 < ncl) { // warp-uniform, at most twice per CTA
                     uint2 *seg = reinterpret_cast<uint2 *>(smem + size_t(s) * stage_bytes + a.in_pad + seg_off);
+                    // this warp's segment ends at the next warp's header offset (or the chunk end)
+                    const int32_t *csx = s_cstart + un.gs * (a.nchunks + 1);
+                    const uint32_t seg_end = warp + 1 < a.gpc
+                                                 ? reinterpret_cast<const uint32_t *>(stage + a.in_pad)[warp + 1]
+                                                 : uint32_t(csx[ch + 1] - csx[ch]);
+                    const int nent = int(seg_end - seg_off) / 8;
                     if (cl1 < ncl) {
                         // end the walk before channel cl1: the first marker reaching it becomes
                         // "end" (this warp's private copy of the segment; the refill overwrites it)
                         int t;
-                        const int j = find_channel(seg, cl1, lane, 9u * R, &t);
+                        const int j = find_channel(seg, nent, cl1, lane, 9u * R, &t);
                         if (lane == 0 && t >= 0) seg[j].y = 9u * R + 1u;
                         __syncwarp();
                     }
@@ -505,7 +499,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
                         // and the window starts at its target (channels cl0..t-1 hold no
                         // nonzeros of this group); none -> start at the end entry
                         int t;
-                        const int j = find_channel(seg, cl0, lane, 9u * R, &t);
+                        const int j = find_channel(seg, nent, cl0, lane, 9u * R, &t);
                         if (t >= 0) {
                             sp += uint32_t(j + 1) * 8u;
                             wp += uint32_t(t) * ch_bytes;
@@ -539,6 +533,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
                 }
                 }
             }
+            SPC_PROF_MARK(3);
             // release stage s: the last warp to finish with it refills it with stage kk + ns.
             // Every warp arrives on the stage's "empty" mbarrier (release); a shared
             // counter picks the last arriver, which waits on that barrier phase
@@ -557,12 +552,14 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
             if (last && kk + ns < total) {
                 if (STG == 0 || lane == 0) fill(kk + ns, s); // (kk + ns) % ns == s
             }
+            SPC_PROF_MARK(0);
             ++kk;
             if (++s == ns) {
                 s = 0;
                 ++rnd;
             }
         }
+        SPC_PROF_MARK(4);
         if (!active) continue;
         if (kind == 1) {
             // park: the partial sums go to slot (b, warp) for CTA b+1
@@ -690,6 +687,24 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         }
     }
     }
+    if (a.sk) {
+        // the last CTA to finish resets the arrival counters for the next launch on
+        // this workspace (every CTA has taken its ticket by then)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(a.sk_ticket + 1, 1u) == gridDim.x - 1) {
+                a.sk_ticket[0] = 0u;
+                a.sk_ticket[1] = 0u;
+                __threadfence();
+            }
+        }
+    }
+    SPC_PROF_MARK(0);
+#ifdef SPC_PROF
+    __syncthreads();
+    if (a.prof && threadIdx.x < 5) atomicAdd(a.prof + threadIdx.x, s_prof[threadIdx.x]);
+#endif
     if (tr && threadIdx.x == 0) tr[2] = gtimer();
 }
 
@@ -707,17 +722,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// SPCONV_PDL=0 launches without programmatic dependent launch (A/B tooling)
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char *e = std::getenv("SPCONV_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
 
 template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG, int EPI = 0>
-cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size_t smem, cudaStream_t s) {
+cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size_t smem, cudaStream_t s,
+                       bool pdl) {
     auto kern = pipe_kernel<R, PT, PS, FUSED, XS, DISP, STG, EPI>;
     static size_t attr_done[64] = {};
     int dev = 0;
@@ -735,7 +743,7 @@ cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, map, a);
@@ -780,6 +788,19 @@ int window_wavefronts(const PipeGeometry &g, int pitch) {
 }
 
 } // namespace
+
+void read_pipe_knobs(PipeKnobs &k) {
+    k = PipeKnobs{};
+    if (const char *e = std::getenv("SPCONV_PIPE_STAGING")) {
+        if (std::strcmp(e, "cp") == 0) k.staging = 2;
+        if (std::strcmp(e, "pad") == 0) k.staging = 1;
+    }
+    if (const char *e = std::getenv("SPCONV_PIPE_SK")) k.sk = e[0] == '1' ? 1 : 0;
+    if (const char *e = std::getenv("SPCONV_PIPE_REV")) k.rev = e[0] == '1';
+    if (const char *e = std::getenv("SPCONV_PDL")) k.pdl = !(e[0] == '0');
+    if (const char *e = std::getenv("SPCONV_PIPE_TRACE")) std::snprintf(k.trace, sizeof(k.trace), "%s", e);
+    if (const char *e = std::getenv("SPCONV_PIPE_PROF")) std::snprintf(k.prof, sizeof(k.prof), "%s", e);
+}
 
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     (void)C; (void)F; (void)H;
@@ -900,19 +921,55 @@ void keep_pool_cached() {
     }
 }
 
-cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
-                        cudaStream_t s, const float *res, int epi) {
+int sm_count_of_current_device() {
+    static int sm_count[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!sm_count[dev & 63]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sm_count[dev & 63] = v;
+    }
+    return sm_count[dev & 63];
+}
+
+// The launch schedule of one forward of N images (staging mode, units, persistent
+// grid, stream-K): the single source of these decisions for launch_pipe and for the
+// spconv_launch_info query the tests assert on.
+bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q) {
+    q = PipeSchedule{};
     // staging: 0 = TMA on the caller's tensor (tile columns shifted by 3),
     //          1 = TMA on a left-padded copy (no shift), 2 = cp.async (fallback)
-    const bool x16 = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const bool x16 = (x & 15) == 0;
     int mode = (p.pipe_tma.ok && x16) ? 0 : p.pipe_pad.ok ? 1 : 2;
-    if (const char *e = std::getenv("SPCONV_PIPE_STAGING")) {
-        if (std::strcmp(e, "cp") == 0) mode = 2;
-        if (std::strcmp(e, "pad") == 0 && p.pipe_pad.ok) mode = 1;
-    }
+    if (p.knobs.staging == 2) mode = 2;
+    if (p.knobs.staging == 1 && p.pipe_pad.ok) mode = 1;
     if (mode != 2 && get_encode() == nullptr) mode = 2;
     const PipeGeometry &g = mode == 0 ? p.pipe_tma : mode == 1 ? p.pipe_pad : p.pipe_cp;
-    if (!g.ok) return cudaErrorInvalidConfiguration;
+    if (!g.ok) return false;
+    q.mode = mode;
+    q.g = &g;
+    const int64_t nblocks = g.band ? (int64_t(N) * g.tiles_y + g.ipb - 1) / g.ipb
+                                   : (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y;
+    q.nunits = nblocks * p.num_gsets;
+    if (q.nunits > 0x7fffffff) return false;
+    // persistent: one CTA per SM (the register file holds one 8-warp CTA)
+    q.grid = int(std::min<int64_t>(q.nunits, sm_count_of_current_device()));
+    // ordered stream-K when the units do not divide evenly over the persistent CTAs
+    // and the last partial round is a noticeable share of the work (c2: 224 units on
+    // 148 SMs = 1.51 rounds -> 2 without it)
+    q.sk = q.nunits > q.grid && q.nunits % q.grid != 0 && q.nunits < 16 * int64_t(q.grid);
+    if (p.knobs.sk >= 0) q.sk = p.knobs.sk == 1 && q.nunits > q.grid;
+    q.launches = mode == 1 ? 2 : 1;
+    return true;
+}
+
+cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
+                        cudaStream_t s, const float *res, int epi) {
+    PipeSchedule sched;
+    if (!pipe_schedule(p, N, reinterpret_cast<uintptr_t>(x), sched)) return cudaErrorInvalidConfiguration;
+    const int mode = sched.mode;
+    const PipeGeometry &g = *sched.g;
     const int Wp = ((p.W + 2) + 3) & ~3;
     float *xp = nullptr;
     if (mode == 1) {
@@ -941,20 +998,8 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.cc = g.cc; a.nchunks = g.nchunks; a.band = g.band;
     a.gpc = p.gpc; a.num_groups = p.num_groups; a.num_gsets = p.num_gsets;
     a.tma = mode != 2 ? 1 : 0;
-    const int64_t nblocks = g.band ? (int64_t(N) * g.tiles_y + g.ipb - 1) / g.ipb
-                                   : (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y;
-    const int64_t nunits = nblocks * p.num_gsets;
-    if (nunits > 0x7fffffff) return cudaErrorInvalidConfiguration;
-    // persistent: one CTA per SM (the register file holds one 8-warp CTA)
-    static int sm_count[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!sm_count[dev & 63]) {
-        int v = 0;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
-        sm_count[dev & 63] = v;
-    }
-    const int64_t grid64 = std::min<int64_t>(nunits, sm_count[dev & 63]);
+    a.ent = 8;
+    const int64_t nunits = sched.nunits;
 
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
@@ -973,48 +1018,54 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
             return cudaErrorInvalidValue;
         }
     }
-    const int grid = int(grid64);
-    // ordered stream-K when the units do not divide evenly over the persistent CTAs
-    // and the last partial round is a noticeable share of the work (c2: 256 units on
-    // 148 SMs = 1.73 rounds -> 2 without it)
-    a.sk = 0; a.sk_part = nullptr; a.sk_flag = nullptr; a.epoch = 0;
-    if (nunits > grid && nunits % grid != 0 && nunits < 16 * int64_t(grid)) a.sk = 1;
-    if (const char *e = std::getenv("SPCONV_PIPE_SK")) a.sk = (e[0] == '1' && nunits > grid) ? 1 : 0;
+    const int grid = sched.grid;
+    a.sk = sched.sk ? 1 : 0; a.sk_part = nullptr; a.sk_flag = nullptr; a.sk_ticket = nullptr; a.epoch = 0;
+    std::unique_lock<std::mutex> ws_lock; // the cached stream-K workspace's lock (see below)
     void *skw = nullptr, *sk_async = nullptr;
     a.trace = nullptr;
-    a.rev = 0;
-    if (const char *e = std::getenv("SPCONV_PIPE_REV")) a.rev = e[0] == '1';
-    const bool tracing = std::getenv("SPCONV_PIPE_TRACE") != nullptr;
+    a.rev = p.knobs.rev;
+    const bool tracing = p.knobs.trace[0] != 0;
     if (tracing && cudaMalloc(&a.trace, size_t(grid) * 64) == cudaSuccess) cudaMemsetAsync(a.trace, 0, size_t(grid) * 64, s);
+    a.prof = nullptr;
+#ifdef SPC_PROF
+    const char *prof_out = p.knobs.prof;
+    if (prof_out[0] && cudaMalloc(&a.prof, 5 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemsetAsync(a.prof, 0, 5 * sizeof(unsigned long long), s);
+#endif
     if (a.sk) {
         static std::atomic<unsigned long long> epochs{0};
         const int qn = p.R * g.T * g.S / 4;
         const size_t part_bytes = size_t(grid) * p.gpc * qn * 32 * sizeof(ulonglong2);
-        const size_t flag_bytes = size_t(grid) * p.gpc * sizeof(unsigned long long);
+        // flags [grid][gpc] u64, then 16 bytes: the arrival ticket and finished-CTA counters
+        const size_t flag_bytes = size_t(grid) * p.gpc * sizeof(unsigned long long) + 16;
         // one workspace per (plan, stream), kept: launches on one stream are ordered
         // (griddepcontrol.wait), launches on different streams never share one.  Under
         // stream capture a stream-ordered allocation is used instead (capturable).
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(s, &cap);
         bool cached = cap == cudaStreamCaptureStatusNone;
-        if (cached) { // at most 8 cached streams per plan (each ~19 MB on c2); others allocate per call
-            Plan &mp = const_cast<Plan &>(p);
-            std::lock_guard<std::mutex> lk(mp.sk_mu);
+        Plan &mp = const_cast<Plan &>(p);
+        if (cached) {
+            // held until the launch is enqueued: a concurrent call on the same stream
+            // cannot replace (free) the workspace between our lookup and our launch
+            ws_lock = std::unique_lock<std::mutex>(mp.sk_mu);
             bool known = false;
             for (auto &w : mp.sk_ws) known |= w.first == s;
-            cached = known || mp.sk_ws.size() < 8;
+            cached = known || mp.sk_ws.size() < 8; // at most 8 cached streams per plan (~19 MB each on c2)
+            if (!cached) ws_lock.unlock();
         }
         if (!cached) {
             keep_pool_cached();
             cudaError_t e = cudaMallocAsync(&skw, part_bytes + flag_bytes, s);
+            if (e == cudaSuccess) // the arrival counters start at 0 (flags never equal a fresh epoch)
+                e = cudaMemsetAsync(static_cast<char *>(skw) + part_bytes + flag_bytes - 16, 0, 16, s);
             if (e != cudaSuccess) {
+                if (skw) cudaFreeAsync(skw, s);
                 if (xp) cudaFreeAsync(xp, s);
                 return e;
             }
             sk_async = skw;
         } else {
-            Plan &mp = const_cast<Plan &>(p);
-            std::lock_guard<std::mutex> lk(mp.sk_mu);
             std::pair<void *, size_t> *ws = nullptr;
             for (auto &w : mp.sk_ws)
                 if (w.first == s) ws = &w.second;
@@ -1036,21 +1087,22 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
                     return e;
                 }
                 ws->second = part_bytes + flag_bytes;
-                // flags start at 0 (never equal to an epoch)
+                // flags and arrival counters start at 0 (flags never equal an epoch)
                 cudaMemsetAsync(static_cast<char *>(ws->first) + part_bytes, 0, flag_bytes, s);
             }
             skw = ws->first;
         }
         a.sk_part = reinterpret_cast<ulonglong2 *>(skw);
         a.sk_flag = reinterpret_cast<unsigned long long *>(static_cast<char *>(skw) + part_bytes);
+        a.sk_ticket = reinterpret_cast<unsigned *>(static_cast<char *>(skw) + part_bytes + flag_bytes - 16);
         // a tagged, process-unique value: stale workspace contents never equal it
         a.epoch = 0x5ec0'0000'0000'0000ull | (++epochs & 0x0000'ffff'ffff'ffffull);
     }
     cudaError_t err = cudaErrorInvalidValue;
 #define SPC_PIPE_MODES(RR, TT, SS, FF, DD, EE)                                                           \
-    err = mode == 0 ? launch_one<RR, TT, SS, FF, 3, DD, 1, EE>(map, a, grid, g.smem_bytes, s)              \
-        : mode == 1 ? launch_one<RR, TT, SS, FF, 0, DD, 1, EE>(map, a, grid, g.smem_bytes, s)              \
-                    : launch_one<RR, TT, SS, FF, 0, DD, 0, EE>(map, a, grid, g.smem_bytes, s);
+    err = mode == 0 ? launch_one<RR, TT, SS, FF, 3, DD, 1, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0)              \
+        : mode == 1 ? launch_one<RR, TT, SS, FF, 0, DD, 1, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0)              \
+                    : launch_one<RR, TT, SS, FF, 0, DD, 0, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0);
     if (p.R == 4 && g.T == 8 && g.S == 4) {
         if (fused) {
             if (p.pipe_dispatch == 1) { SPC_PIPE_MODES(4, 8, 4, true, 1, 0) }
@@ -1077,7 +1129,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
         unsigned long long t0 = ~0ull;
         for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[size_t(b) * 8]);
-        if (FILE *f = std::fopen(std::getenv("SPCONV_PIPE_TRACE"), "a")) {
+        if (FILE *f = std::fopen(p.knobs.trace, "a")) {
             for (int b = 0; b < grid; ++b) {
                 const unsigned long long *e = &h[size_t(b) * 8];
                 auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
@@ -1089,6 +1141,20 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         }
         cudaFree(a.trace);
     }
+#ifdef SPC_PROF
+    if (a.prof) {
+        // diagnostic: one line per launch: grid, warps, phase cycle sums (see the kernel)
+        unsigned long long h[5];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost);
+        if (FILE *f = std::fopen(prof_out, "a")) {
+            std::fprintf(f, "grid %d warps %d other %llu wait %llu walk %llu release %llu epilogue %llu\n", grid,
+                         grid * p.gpc, h[0], h[1], h[2], h[3], h[4]);
+            std::fclose(f);
+        }
+        cudaFree(a.prof);
+    }
+#endif
     if (sk_async) {
         cudaError_t e2 = cudaFreeAsync(sk_async, s);
         if (err == cudaSuccess) err = e2;

@@ -318,6 +318,26 @@ bool tiled_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     return K == 3 && stride == 1 && pad == 1 && H >= 1 && W >= 1 && W + 8 <= 4096;
 }
 
+// The tiled kernel's staging ring must fit the device's opt-in shared memory (very wide
+// rows do not: W = 3300 needs ~238 KB); checked at create so AUTO can fall back to the
+// generic kernel instead of failing every forward.
+bool tiled_fits(int C, int H, int W, int F, int K, int stride, int pad, int device) {
+    if (!tiled_supported(C, H, W, F, K, stride, pad)) return false;
+    Plan tmp;
+    tmp.C = C; tmp.H = H; tmp.W = W; tmp.F = F; tmp.K = K; tmp.stride = stride; tmp.pad = pad;
+    tmp.Ho = (H + 2 * pad - K) / stride + 1;
+    tmp.Wo = (W + 2 * pad - K) / stride + 1;
+    tmp.R = 4;
+    tmp.num_groups = (F + 3) / 4;
+    tiled_geometry(tmp);
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) {
+        cudaGetLastError();
+        optin = 227 * 1024;
+    }
+    return tmp.geo.smem_bytes + 1024 <= size_t(optin); // + the kernel's static barriers
+}
+
 int tiled_default_R(int C, int F, double density) {
     (void)C; (void)density;
     return F >= 8 ? 8 : 4;

@@ -82,6 +82,7 @@ void free_plan(Plan *p) {
     cudaFree(p->d_stream);
     cudaFree(p->d_chunk_start);
     cudaFree(p->d_stream2);
+    cudaFree(p->d_wdense);
     for (auto &w : p->sk_ws) cudaFree(w.second.first);
     cudaFree(p->d_xbuf);
     cudaFree(p->d_ybuf);
@@ -397,7 +398,7 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
     if (Hp < K || Wp < K) return SPCONV_ERR_SHAPE;
     spconv_options_t o{};
     if (opts) o = *opts;
-    if (o.kernel < SPCONV_KERNEL_AUTO || o.kernel > SPCONV_KERNEL_PIPE) return SPCONV_ERR_UNSUPPORTED;
+    if (o.kernel < SPCONV_KERNEL_AUTO || o.kernel > SPCONV_KERNEL_DENSE) return SPCONV_ERR_UNSUPPORTED;
     for (int r : o.reserved)
         if (r != 0) return SPCONV_ERR_UNSUPPORTED;
 
@@ -444,16 +445,27 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
     p->Wo = (Wp - K) / stride + 1;
     p->nnz = nnz;
     p->device = device;
-    const bool tiled_ok = spconv::tiled_supported(C, H, W, F, K, stride, pad);
+    spconv::read_pipe_knobs(p->knobs); // debug / A/B knobs: read once, here
+    const bool tiled_ok = spconv::tiled_fits(C, H, W, F, K, stride, pad, device);
     const bool pipe_ok = spconv::pipe_supported(C, H, W, F, K, stride, pad);
-    if ((o.kernel == SPCONV_KERNEL_TILED && !tiled_ok) || (o.kernel == SPCONV_KERNEL_PIPE && !pipe_ok)) {
+    const bool dense_ok = spconv::dense_supported(C, H, W, F, K, stride, pad);
+    if ((o.kernel == SPCONV_KERNEL_TILED && !tiled_ok) || (o.kernel == SPCONV_KERNEL_PIPE && !pipe_ok) ||
+        (o.kernel == SPCONV_KERNEL_DENSE && !dense_ok)) {
         delete p;
         return SPCONV_ERR_UNSUPPORTED;
     }
-    if (o.kernel == SPCONV_KERNEL_AUTO)
+    const double density = double(nnz) / (double(F) * ncol);
+    if (o.kernel == SPCONV_KERNEL_AUTO) {
         p->kernel = pipe_ok ? SPCONV_KERNEL_PIPE : tiled_ok ? SPCONV_KERNEL_TILED : SPCONV_KERNEL_GENERIC;
-    else
+        // the dense kernel at and above the measured break-even density (DESIGN.md NEXT-1)
+        p->dense = dense_ok && density >= spconv::kDenseBreakEven;
+    } else if (o.kernel == SPCONV_KERNEL_DENSE) {
+        // fused / epilogue calls of a dense plan take AUTO's sparse kernel
+        p->kernel = pipe_ok ? SPCONV_KERNEL_PIPE : tiled_ok ? SPCONV_KERNEL_TILED : SPCONV_KERNEL_GENERIC;
+        p->dense = true;
+    } else {
         p->kernel = o.kernel;
+    }
     int R = o.rows_per_group;
     if (R == 0) {
         R = p->kernel == SPCONV_KERNEL_PIPE ? 4 : spconv::tiled_default_R(C, F, double(nnz) / (double(F) * ncol));
@@ -472,6 +484,16 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
         return SPCONV_ERR_UNSUPPORTED;
     }
     st = build_plan(p, h_rowptr, h_colidx, h_values, h_bias, R);
+    if (!st && p->dense) {
+        spconv::dense_geometry(*p, p->dense_geo);
+        if (!p->dense_geo.ok) {
+            if (o.kernel == SPCONV_KERNEL_DENSE) st = SPCONV_ERR_UNSUPPORTED;
+            p->dense = false;
+        } else {
+            const std::vector<float> w = spconv::dense_weights(*p, p->dense_geo, h_rowptr, h_colidx, h_values);
+            st = upload(&p->d_wdense, w.data(), w.size(), p->device_bytes);
+        }
+    }
     if (st) {
         free_plan(p);
         return st;
@@ -520,7 +542,9 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e;
     const int epi = fused ? 0 : flags;
-    if (p->kernel == SPCONV_KERNEL_PIPE && !(epi && p->pipe_dispatch == 1))
+    if (p->dense && !fused && epi == 0)
+        e = spconv::launch_dense(*p, N, x, y, s);
+    else if (p->kernel == SPCONV_KERNEL_PIPE && !(epi && p->pipe_dispatch == 1))
         e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s, res, epi);
     else if (p->kernel == SPCONV_KERNEL_TILED && epi == 0)
         e = spconv::launch_tiled(*p, N, x, y, argmax, fused, s);
@@ -703,6 +727,47 @@ int spconv_output_dims(spconv_plan_t plan, int N, int fused, int64_t dims[4]) {
     return SPCONV_OK;
 }
 
+int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spconv_launch_info_t *info) {
+    if (!plan || !info) return SPCONV_ERR_NULLPTR;
+    if (N < 0) return SPCONV_ERR_SHAPE;
+    Plan *p = plan;
+    *info = spconv_launch_info_t{};
+    info->kernel = p->kernel;
+    info->rows_per_group = p->R;
+    info->launches = N > 0 ? 1 : 0;
+    (void)fused;
+    if (p->dense && !fused && N > 0) {
+        const spconv::DenseGeometry &g = p->dense_geo;
+        info->kernel = SPCONV_KERNEL_DENSE;
+        info->rows_per_group = 8;
+        const int64_t blocks = g.ipb > 1 ? (N + g.ipb - 1) / g.ipb : int64_t(N) * g.bpi;
+        info->units = blocks * g.fsets;
+        DeviceGuard guard(p->device);
+        if (!guard.ok) return SPCONV_ERR_CUDA;
+        info->grid = int(std::min<int64_t>(info->units, spconv::sm_count_of_current_device()));
+        info->staging = (g.padded || (reinterpret_cast<uintptr_t>(x) & 15)) ? 1 : 0;
+        info->channels_per_stage = g.cc;
+        info->stages = g.nstage;
+        info->launches = info->staging ? 2 : 1;
+        return SPCONV_OK;
+    }
+    if (p->kernel == SPCONV_KERNEL_PIPE && N > 0) {
+        DeviceGuard guard(p->device);
+        if (!guard.ok) return SPCONV_ERR_CUDA;
+        spconv::PipeSchedule q;
+        if (!spconv::pipe_schedule(*p, N, reinterpret_cast<uintptr_t>(x), q)) return SPCONV_ERR_UNSUPPORTED;
+        info->grid = q.grid;
+        info->stream_k = q.sk ? 1 : 0;
+        info->units = q.nunits;
+        info->band = q.g->band;
+        info->staging = q.mode;
+        info->channels_per_stage = q.g->cc;
+        info->stages = q.g->nstage;
+        info->launches = q.launches;
+    }
+    return SPCONV_OK;
+}
+
 int spconv_plan_info(spconv_plan_t plan, spconv_plan_info_t *info) {
     if (!plan || !info) return SPCONV_ERR_NULLPTR;
     const Plan *p = plan;
@@ -711,13 +776,14 @@ int spconv_plan_info(spconv_plan_t plan, spconv_plan_info_t *info) {
     info->stride = p->stride; info->pad = p->pad; info->Ho = p->Ho; info->Wo = p->Wo;
     info->nnz = p->nnz;
     info->device = p->device;
-    info->kernel = p->kernel;
+    info->kernel = p->dense ? SPCONV_KERNEL_DENSE : p->kernel; // the kernel of conv-only calls
     info->rows_per_group = p->R;
     info->num_groups = p->num_groups;
     info->device_bytes = p->device_bytes;
-    // the pipelined kernel needs a padding pass first when TMA cannot stage the
+    // the pipelined / dense kernels need a padding pass first when TMA cannot stage the
     // caller's rows (W % 4 != 0); a misaligned base pointer adds it at run time
-    info->launches_per_call = (p->kernel == SPCONV_KERNEL_PIPE && !p->pipe_tma.ok) ? 2 : 1;
+    info->launches_per_call = p->dense ? (p->dense_geo.padded ? 2 : 1)
+                                       : (p->kernel == SPCONV_KERNEL_PIPE && !p->pipe_tma.ok) ? 2 : 1;
     return SPCONV_OK;
 }
 

@@ -63,6 +63,35 @@ struct PipeGeometry {
     size_t smem_bytes;       // dynamic shared memory per CTA
 };
 
+// Debug / A/B knobs of the pipe kernel, read from the environment ONCE, when the
+// plan is created (no getenv on the forward path).
+struct PipeKnobs {
+    int staging = -1;     // SPCONV_PIPE_STAGING: -1 auto, 1 padded copy, 2 cp.async
+    int sk = -1;          // SPCONV_PIPE_SK: -1 auto, 0 off, 1 on (when there are more units than CTAs)
+    int rev = 0;          // SPCONV_PIPE_REV=1: reversed work order (debug)
+    int pdl = 1;          // SPCONV_PDL=0: launch without programmatic dependent launch
+    char trace[256] = {}; // SPCONV_PIPE_TRACE=<file>: per-CTA timestamps (debug, synchronises)
+    char prof[256] = {};  // SPCONV_PIPE_PROF=<file>: phase clock sums (-DSPC_PROF builds only)
+};
+void read_pipe_knobs(PipeKnobs &k);
+
+// Geometry of the dense FP32 direct-conv kernel (kernel_dense.cu, NEXT-1).
+struct DenseGeometry {
+    bool ok = false;
+    int S = 0;                // lane tile columns (7 or 8); rows are 2
+    int LR = 0, LY = 0;       // lanes per staged row, lane rows per warp
+    int RY = 0;               // lane rows per image = ceil(Ho / 2)
+    int ipb = 0, bpi = 0;     // images per unit (small images) / units per image
+    int rows = 0;             // staged rows per image slot (incl. the 2 halo rows)
+    int pitch = 0;            // smem words per staged row (bank-conflict-free choice)
+    int cc = 0, nchunks = 0, nstage = 0;
+    int in_bytes = 0, w_bytes = 0, stage_bytes = 0;
+    int fsets = 0;            // 64-output-channel sets
+    int padded = 0, wq = 0;   // TMA on a right-padded copy (row stride not 16-byte aligned), its row length
+    int xoff = 0;             // smem column of image column 0
+    size_t smem_bytes = 0;
+};
+
 struct Plan {
     int C, H, W, F, K, stride, pad, Ho, Wo;
     int64_t nnz;
@@ -89,6 +118,12 @@ struct Plan {
     int32_t *d_chunk_start = nullptr; // [num_gsets * (nchunks + 1)] byte offsets into d_stream2
     uint4 *d_stream2 = nullptr;    // chunks: header (GPC u32 byte offsets) + 16-byte entries
     PipeGeometry pipe_tma{}, pipe_pad{}, pipe_cp{};
+    PipeKnobs knobs{};
+    // dense path (NEXT-1): conv-only calls of a plan whose kernel is SPCONV_KERNEL_DENSE
+    // run the dense kernel on the densified filters; fused / epilogue calls use the pipe
+    bool dense = false;
+    float *d_wdense = nullptr;
+    DenseGeometry dense_geo{};
     int64_t device_bytes = 0;
     // spconv_forward_host staging
     std::mutex host_mu;
@@ -120,15 +155,37 @@ void keep_pool_cached();
 cudaError_t launch_resize(const float *x, float *y, int64_t planes, int Hin, int Win, int Hout, int Wout,
                           cudaStream_t s);
 
+// kernel_pipe.cu: the launch schedule of one forward (spconv_launch_info reports it)
+struct PipeSchedule {
+    int mode = 0;                       // 0 TMA on x, 1 TMA on a left-padded copy, 2 cp.async
+    const PipeGeometry *g = nullptr;
+    int64_t nunits = 0;                 // (pixel block, group set) work units
+    int grid = 0;                       // persistent CTAs
+    bool sk = false;                    // ordered stream-K split of the units over the CTAs
+    int launches = 1;                   // kernel launches per call
+};
+bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q);
+int sm_count_of_current_device();
+
 // kernel_pipe.cu
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad);
 void pipe_geometry(const Plan &p, int mode, PipeGeometry &g); // mode: 0 TMA, 1 TMA on padded copy, 2 cp.async
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                         bool fused, cudaStream_t s, const float *res = nullptr, int epi = 0);
 
+// kernel_dense.cu.  AUTO routes conv-only calls of layers at or above this density to
+// the dense kernel (the measured B200 break-even, DESIGN.md NEXT-1).
+constexpr double kDenseBreakEven = 0.55;
+bool dense_supported(int C, int H, int W, int F, int K, int stride, int pad);
+void dense_geometry(const Plan &p, DenseGeometry &g);
+std::vector<float> dense_weights(const Plan &p, const DenseGeometry &g, const std::vector<int32_t> &rowptr,
+                                 const std::vector<int32_t> &colidx, const std::vector<float> &values);
+cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStream_t s);
+
 // kernel_tiled.cu
 bool tiled_supported(int C, int H, int W, int F, int K, int stride, int pad);
 int tiled_default_R(int C, int F, double density);
+bool tiled_fits(int C, int H, int W, int F, int K, int stride, int pad, int device);
 void tiled_geometry(Plan &p); // fills p.geo for p.R
 cudaError_t launch_tiled(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                          bool fused, cudaStream_t s);

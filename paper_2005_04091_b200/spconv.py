@@ -19,15 +19,16 @@ LIB_PATH = os.environ.get("SPCONV_LIB") or os.path.join(_PKG, "libspconv.so")
 SPCONV_OK = 0
 STATUS = {0: "OK", -1: "NULLPTR", -2: "SHAPE", -3: "CSR", -4: "UNSUPPORTED", -5: "ALIGN",
           -6: "DEVICE", -7: "CUDA", -8: "OOM", -9: "ALIAS"}
-KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TILED, KERNEL_PIPE = 0, 1, 2, 3
-KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED, "pipe": KERNEL_PIPE}
+KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TILED, KERNEL_PIPE, KERNEL_DENSE = 0, 1, 2, 3, 4
+KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED, "pipe": KERNEL_PIPE,
+           "dense": KERNEL_DENSE}
 
 # Every symbol include/spconv.h declares (checked by tests/test_abi.py).
 EXPORTS = ("spconv_create", "spconv_create_ex", "spconv_forward", "spconv_fused_relu_maxpool",
            "spconv_forward_host", "spconv_destroy", "spconv_output_dims", "spconv_plan_info",
            "spconv_status_string", "spconv_abi_version", "spconv_debug_decoded",
            "spconv_last_cuda_error", "spconv_forward_ex", "spconv_resize_bilinear",
-           "spconv_resize_fused_relu_maxpool")
+           "spconv_resize_fused_relu_maxpool", "spconv_launch_info")
 
 
 class SpconvError(RuntimeError):
@@ -53,6 +54,13 @@ class PlanInfo(ctypes.Structure):
                 ("launches_per_call", ctypes.c_int)]
 
 
+class LaunchInfo(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int), ("rows_per_group", ctypes.c_int), ("grid", ctypes.c_int),
+                ("stream_k", ctypes.c_int), ("units", ctypes.c_int64), ("band", ctypes.c_int),
+                ("staging", ctypes.c_int), ("channels_per_stage", ctypes.c_int), ("stages", ctypes.c_int),
+                ("launches", ctypes.c_int), ("reserved", ctypes.c_int * 7)]
+
+
 _lib = None
 
 
@@ -76,6 +84,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.spconv_destroy.argtypes = [vp]
     lib.spconv_output_dims.argtypes = [vp, I, I, ctypes.POINTER(ctypes.c_int64)]
     lib.spconv_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+    lib.spconv_launch_info.argtypes = [vp, I, I, vp, ctypes.POINTER(LaunchInfo)]
     lib.spconv_status_string.argtypes = [I]
     lib.spconv_status_string.restype = ctypes.c_char_p
     lib.spconv_abi_version.argtypes = []
@@ -198,6 +207,14 @@ def spconv_plan_info(plan) -> dict:
     return {f: getattr(info, f) for f, _ in PlanInfo._fields_}
 
 
+def spconv_launch_info(plan, N, fused=False, x_ptr=None) -> dict:
+    """The launch schedule a forward of N images would use (stream-K, grid, units, ...)."""
+    info = LaunchInfo()
+    _check(load_library().spconv_launch_info(plan, N, int(bool(fused)), x_ptr, ctypes.byref(info)),
+           "spconv_launch_info")
+    return {f: getattr(info, f) for f, _ in LaunchInfo._fields_ if f != "reserved"}
+
+
 def spconv_debug_decoded(plan, nnz):
     c, dy, dx = (np.empty(nnz, np.int32) for _ in range(3))
     _check(load_library().spconv_debug_decoded(plan, _ptr(c), _ptr(dy), _ptr(dx)), "spconv_debug_decoded")
@@ -306,6 +323,9 @@ class SparseConv2d:
         am = np.empty(y.shape, np.int32) if (fused and with_argmax) else None
         spconv_forward_host(self.plan, N, x, y, fused, am)
         return (y, am) if fused else y
+
+    def launch_info(self, N, fused=False, x=None):
+        return spconv_launch_info(self.plan, N, fused, None if x is None else x.data_ptr())
 
     def debug_decoded(self):
         return spconv_debug_decoded(self.plan, self.nnz)

@@ -50,9 +50,14 @@ def main():
     print("c2 pipe cp.async", "ok" if ok else "MISMATCH")
     good &= ok
     del os.environ["SPCONV_PIPE_STAGING"]
-    # R = 2 rows per group (11-12 warps per CTA), incl. ordered stream-K (c2 N=19)
+    # ordered stream-K at R = 4 (c2 N=23: 162 units on 148 CTAs, arrival tickets,
+    # park / resume, walks split inside a stage)
+    ok = check(synthgen.CONFIGS["c2"].with_batch(23), "pipe")
+    print("c2 23 pipe R=4 stream-K", "ok" if ok else "MISMATCH", flush=True)
+    good &= ok
+    # R = 2 rows per group (11-12 warps per CTA), incl. ordered stream-K (c2 N=23)
     os.environ["SPCONV_PIPE_R"] = "2"
-    for name, N in (("c2", 2), ("c2", 19), ("c4_50", 2)):
+    for name, N in (("c2", 2), ("c2", 23), ("c4_50", 2)):
         ok = check(synthgen.CONFIGS[name].with_batch(N), "pipe")
         print(name, N, "pipe R=2", "ok" if ok else "MISMATCH", flush=True)
         good &= ok

@@ -8,11 +8,14 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(extra_env=None):
+def _run(extra_env=None, gpus=1, drop_world=False):
     env = dict(os.environ, **(extra_env or {}))
+    if drop_world:
+        for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+            env.pop(k, None)
     return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config",
-                           "c1", "--steps", "3", "--warmup", "3"], capture_output=True, text=True, env=env,
-                          cwd=ROOT, timeout=600)
+                           "c1", "--steps", "3", "--warmup", "3", "--gpus", str(gpus)], capture_output=True,
+                          text=True, env=env, cwd=ROOT, timeout=600)
 
 
 def test_reference_arm_json_line():
@@ -31,6 +34,20 @@ def test_reference_arm_json_line():
 
 
 def test_reference_arm_silent_on_other_ranks():
-    r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, gpus=2)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def test_gpus_flag_without_torchrun_prints_one_line():
+    """`bench.py --gpus 2` outside torchrun: the reference arm runs once (rank 0's work)
+    and reports n_gpus = 2 (the native arm spawns 2 ranks itself)."""
+    r = _run(gpus=2, drop_world=True)
+    assert r.returncode == 0, r.stderr
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_gpus_flag_must_match_world_size():
+    r = _run({"RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"}, gpus=4)
+    assert r.returncode != 0 and "disagrees" in r.stderr

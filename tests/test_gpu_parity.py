@@ -45,7 +45,10 @@ def _bias(cfg):
     return synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3))
 
 
-def _check_full(cfg, kernel, fused, N=None, integer=False):
+def _check_full(cfg, kernel, fused, N=None, integer=False, stream_k=None, f64=True):
+    """Element-by-element bitwise comparison with the FP32-ordered oracle.  stream_k
+    (True/False): assert the launch schedule (spconv_launch_info, the launch's own
+    decision code) really does / does not split units with ordered stream-K."""
     if N is not None:
         cfg = cfg.with_batch(N)
     L = synthgen.make_layer(cfg, integer=integer)
@@ -53,6 +56,12 @@ def _check_full(cfg, kernel, fused, N=None, integer=False):
     b = synthgen.make_bias(cfg.F, synthgen.seed_of(cfg.k, 3), integer=integer)
     layer = _layer(cfg, c, b, kernel)
     x = torch.from_numpy(L.x).cuda()
+    if stream_k is not None:
+        info = layer.launch_info(cfg.N, fused, x)
+        assert info["kernel"] == 3, info
+        assert bool(info["stream_k"]) == stream_k, info
+        if stream_k:
+            assert info["units"] > info["grid"], info
     args = (L.x, cfg.F, cfg.K, cfg.stride, cfg.pad, c.rowptr, c.colidx, c.values, b)
     if not fused:
         y = layer(x).cpu().numpy()
@@ -60,8 +69,9 @@ def _check_full(cfg, kernel, fused, N=None, integer=False):
         assert y.shape == ref.shape
         mism = np.count_nonzero(bits(y) != bits(ref))
         assert mism == 0, f"{mism} of {y.size} outputs differ bitwise"
-        ok, worst = allclose_contract(y, oracle.conv_f64(*args))
-        assert ok, worst
+        if f64:
+            ok, worst = allclose_contract(y, oracle.conv_f64(*args))
+            assert ok, worst
     else:
         p, am = layer.fused_relu_maxpool(x)
         p, am = p.cpu().numpy(), am.cpu().numpy()
@@ -211,6 +221,26 @@ def test_unaligned_input_uses_cp_async_path(kernel):
     y = layer(x).cpu().numpy()
     ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, None)
     assert np.array_equal(bits(y), bits(ref))
+
+
+def test_very_wide_rows_fall_back_when_tiled_does_not_fit():
+    """W = 3300: the tiled kernel's staging ring would need more than the 227 KB of opt-in
+    shared memory, so AUTO must pick the generic kernel at create (not fail every
+    forward) and an explicit tiled request is rejected as unsupported."""
+    from paper_2005_04091_b200 import SparseConv2d
+    from paper_2005_04091_b200.spconv import SpconvError
+    cfg = synthgen.LayerConfig(9, "wide", 1, 2, 3, 3300, 3, 3, 1, 1, 0.5, False, True)
+    L = synthgen.make_layer(cfg)
+    c, b = L.csr, _bias(cfg)
+    layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, device=0)
+    assert layer.info["kernel"] == 1  # generic
+    y = layer(torch.from_numpy(L.x).cuda()).cpu().numpy()
+    ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+    assert np.array_equal(bits(y), bits(ref))
+    layer.close()
+    with pytest.raises(SpconvError):
+        SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, device=0,
+                     kernel="tiled")
 
 
 def test_batch_zero_is_noop_and_errors():
@@ -363,6 +393,7 @@ def test_stream_k_workspace_per_stream_and_back_to_back_launches():
     c = L.csr
     layer = _layer(cfg, c, None, "auto")
     x = torch.from_numpy(L.x).cuda()
+    assert layer.launch_info(cfg.N, False, x)["stream_k"] == 1
     x2 = torch.flip(x, dims=[0]).contiguous()
     ref, ref2 = layer(x), layer(x2)
     streams = [torch.cuda.Stream() for _ in range(10)]
@@ -403,21 +434,69 @@ def test_pipe_staging_paths(staging, name, fused, N, monkeypatch):
 
 
 @pytest.mark.parametrize("sk", ["auto", "1", "0"])
-@pytest.mark.parametrize("name,fused,N", [("c2", False, 19), ("c3", True, 23), ("c4_95", False, 76)])
+@pytest.mark.parametrize("name,fused,N", [("c2", False, 23), ("c2", False, 32), ("c3", True, 23),
+                                          ("c4_95", False, 76)])
 def test_pipe_ordered_stream_k(sk, name, fused, N, monkeypatch):
-    """More units than persistent CTAs (c2 N=19: 152 units on 148 SMs): with ordered
-    stream-K a unit cut by a CTA's range is started by one CTA, parked, and finished by
-    the next -- still one ascending fma chain per output, so the bits equal the oracle's
-    with stream-K on, off, and chosen automatically."""
+    """More units than persistent CTAs (c2 N=23: 2 group sets x 81 band units = 162 on
+    148 SMs; N=32, the bench batch: 224): with ordered stream-K a unit cut by a CTA's
+    range is started by one CTA, parked, and finished by the next -- still one ascending
+    fma chain per output, so the bits equal the oracle's with stream-K forced on, off,
+    and chosen automatically.  The launch schedule is asserted, not assumed."""
     if sk != "auto":
         monkeypatch.setenv("SPCONV_PIPE_SK", sk)
-    _check_full(synthgen.CONFIGS[name], "auto", fused, N=N)
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N, stream_k=(sk != "0"), f64=False)
 
 
 def test_pipe_ordered_stream_k_mask_dispatcher(monkeypatch):
+    """The mask dispatcher under stream-K: heads that end and tails that start inside a
+    stage (mask_walk's cl0/cl1 partial-stage path)."""
     monkeypatch.setenv("SPCONV_PIPE_SK", "1")
     monkeypatch.setenv("SPCONV_PIPE_DISPATCH", "mask")
-    _check_full(synthgen.CONFIGS["c2"], "pipe", False, N=19)
+    _check_full(synthgen.CONFIGS["c2"], "pipe", False, N=23, stream_k=True, f64=False)
+    _check_full(synthgen.CONFIGS["c3"], "pipe", True, N=23, stream_k=True)
+
+
+def test_bench_configuration_c2_elementwise():
+    """The exact bench launch (c2, N=32, AUTO: pipe, R = 4, band units, ordered
+    stream-K over 148 CTAs) against the oracle, ALL 6.4 M outputs bitwise (plus the
+    FP64 contract)."""
+    _check_full(synthgen.CONFIGS["c2"], "auto", False, stream_k=True)
+
+
+def test_bench_configuration_c3_elementwise():
+    """c3 at its BASELINE.json batch (N=32, fused bias+ReLU+2x2 maxpool, 90% sparsity,
+    stream-K engaged): every pooled value and argmax bitwise."""
+    _check_full(synthgen.CONFIGS["c3"], "auto", True, stream_k=True)
+
+
+def test_stream_k_forward_progress_beside_a_concurrent_gemm():
+    """Stream-K CTAs take their work index from an arrival ticket, so a tail only ever
+    waits for the head of a CTA that is already running.  Here the conv launches (two
+    streams) start while cuBLAS GEMMs hold most SMs (a third stream): CTAs become
+    resident in an arbitrary order; the launches must finish (bounded by the test's
+    own timeout) with the oracle's bits."""
+    cfg = synthgen.CONFIGS["c2"]
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    layer = _layer(cfg, c, None, "auto")
+    x = torch.from_numpy(L.x).cuda()
+    assert layer.launch_info(cfg.N, False, x)["stream_k"] == 1
+    ref = layer(x)
+    a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    sg, s1, s2 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    torch.cuda.synchronize()
+    with torch.cuda.stream(sg):
+        for _ in range(4):
+            a = (a @ a).clamp_(-1, 1)
+    for s in (s1, s2):
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                outs.append(layer(x))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.view(torch.int32), ref.view(torch.int32))
+    layer.close()
 
 
 # ---------------------------------------------------------------- NEXT-3: epilogues and blocks
@@ -595,15 +674,15 @@ def test_pipe_tuning_options_keep_the_bits(env, monkeypatch):
     _check_full(synthgen.CONFIGS["c3"], "pipe", True, N=2)
 
 
-@pytest.mark.parametrize("name,fused,N", [("c1", False, 1), ("c2", False, 2), ("c3", True, 2), ("c2", False, 19),
+@pytest.mark.parametrize("name,fused,N", [("c1", False, 1), ("c2", False, 2), ("c3", True, 2), ("c2", False, 23),
                                           ("c4_50", False, 3), ("c4_95", False, 76), ("c5", False, 1)])
 def test_pipe_two_rows_per_group(name, fused, N, monkeypatch):
     """Pipelined kernel with R = 2 rows per group (11-12 warps per CTA instead of 8,
     group sets spread evenly; SPCONV_PIPE_R=2): only the grouping changes, every output
     row is still one ascending fma chain -- bits equal to the oracle, stream-K included
-    (c2 N=19, c4_95 N=76)."""
+    (c2 N=23, c4_95 N=76: asserted)."""
     monkeypatch.setenv("SPCONV_PIPE_R", "2")
-    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N)
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N, stream_k=True if N in (23, 76) else None)
     _check_full(synthgen.CONFIGS[name], "pipe", fused, N=1, integer=True)
 
 
@@ -646,11 +725,12 @@ def test_pipe_auto_rows_per_group(name, density, want_R, monkeypatch):
 def test_pipe_skipped_channels_with_stream_k_splits(keep, sk, R, monkeypatch):
     """Rows with nonzeros only in every keep-th input channel (long runs of channels
     with no nonzero for a group, which the walk skips in one step), with ordered
-    stream-K (c2 shape, N=19: splits land at arbitrary channels, also inside skipped
-    runs) and without, at R = 4 and R = 2 -- bits equal to the oracle."""
+    stream-K (c2 shape, N=23: 162 units at R = 4, 243 at R = 2, so splits land at
+    arbitrary channels, also inside skipped runs; asserted) and without, at R = 4 and
+    R = 2 -- bits equal to the oracle."""
     monkeypatch.setenv("SPCONV_PIPE_SK", sk)
     monkeypatch.setenv("SPCONV_PIPE_R", R)
-    cfg = synthgen.CONFIGS["c2"].with_batch(19)
+    cfg = synthgen.CONFIGS["c2"].with_batch(23)
     L = synthgen.make_layer(cfg.with_density(0.5))
     c = L.csr
     rows, cols, vals = [0], [], []
@@ -665,6 +745,8 @@ def test_pipe_skipped_channels_with_stream_k_splits(keep, sk, R, monkeypatch):
                        np.array(vals, np.float32))
     b = _bias(cfg)
     layer = _layer(cfg, csr, b, "pipe")
+    info = layer.launch_info(cfg.N)
+    assert info["rows_per_group"] == int(R) and bool(info["stream_k"]) == (sk == "1"), info
     y = layer(torch.from_numpy(L.x).cuda()).cpu().numpy()
     ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b)
     assert np.array_equal(bits(y), bits(ref))
@@ -682,3 +764,57 @@ def test_forward_host_chunk_counts(monkeypatch):
         monkeypatch.setenv("SPCONV_HOST_CHUNKS", k)
         assert np.array_equal(bits(layer.forward_host(L.x)), bits(ref)), k
     layer.close()
+
+
+# ---------------------------------------------------------------- NEXT-1: the dense kernel
+@pytest.mark.parametrize("name,N,density", [("c2", 2, 1.0), ("c2", 3, 0.2), ("c4_50", 3, 0.5), ("c5", 1, 0.6),
+                                            ("c1", 2, 1.0)])
+def test_dense_kernel_bitwise(name, N, density):
+    """The dense FP32 direct conv of the densified filters (kernel="dense") gives the
+    FP32-ordered oracle's bits at any density (a zero tap is an exact no-op), incl.
+    the right-padded staging copy (c4: 56-byte rows) and small images packed per unit;
+    fused calls on the same plan run the pipe kernel."""
+    cfg = synthgen.CONFIGS[name].with_density(density)
+    _check_full(cfg, "dense", False, N=N)
+    _check_full(cfg, "dense", True, N=N)
+
+
+def test_dense_kernel_random_shapes():
+    """Seeded random K=3 layers through the dense kernel: widths 1..248 (lanes per row
+    1..32, 7 or 8 columns per lane, images packed per unit), F not a multiple of 64,
+    C not a multiple of the channels per stage, bias on/off -- bitwise."""
+    from paper_2005_04091_b200 import SparseConv2d
+    rng = np.random.default_rng(2024)
+    for i in range(24):
+        C = int(rng.integers(1, 40))
+        F = int(rng.integers(1, 140))
+        H = int(rng.integers(1, 40))
+        W = int(rng.choice([1, 3, 8, 14, 16, 28, 33, 56, 57, 64, 100, 112, 124, 160, 200, 248]))
+        N = int(rng.integers(1, 4))
+        d = float(rng.choice([0.05, 0.3, 0.7, 1.0]))
+        cfg = synthgen.LayerConfig(7, "rnd", N, C, H, W, F, 3, 1, 1, d, False, True)
+        L = synthgen.make_layer(cfg)
+        c = L.csr
+        b = _bias(cfg) if i % 2 else None
+        layer = SparseConv2d(C, H, W, F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, device=0, kernel="dense")
+        assert layer.info["kernel"] == 4
+        y = layer(torch.from_numpy(L.x).cuda()).cpu().numpy()
+        ref = oracle.conv_f32(L.x, F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+        assert np.array_equal(bits(y), bits(ref)), (i, N, C, H, W, F, d)
+        layer.close()
+
+
+def test_auto_routes_dense_layers_to_the_dense_kernel():
+    """AUTO: conv-only calls of layers at or above the measured break-even density run the
+    dense kernel (plan and launch info say so), sparser layers the pipe kernel."""
+    from paper_2005_04091_b200 import spconv
+    from paper_2005_04091_b200.spconv import SparseConv2d
+    for d, want in ((1.0, 4), (0.2, 3)):
+        cfg = synthgen.CONFIGS["c2"].with_density(d).with_batch(2)
+        L = synthgen.make_layer(cfg)
+        layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, L.csr.rowptr, L.csr.colidx, L.csr.values,
+                             device=0)
+        assert layer.info["kernel"] == want
+        assert layer.launch_info(2)["kernel"] == want
+        assert layer.launch_info(2, fused=True)["kernel"] == 3
+        layer.close()

@@ -229,6 +229,29 @@ def test_points_match_full():
     assert np.array_equal(a2, amf[tuple(pts2.T)])
 
 
+@pytest.mark.parametrize("name,N,stride,pad", [("c1", 1, 1, 1), ("c2", 1, 1, 1), ("c1", 2, 2, 0)])
+def test_points_f64_vs_torch_conv2d(name, N, stride, pad):
+    """oracle_conv_points_f64 (the FP64 tolerance reference of the full-size sampled GPU
+    tests) against torch.nn.functional.conv2d in float64 on the densified filters (a
+    library routine, PAPER.md L308-330 semantics), at sampled points incl. all borders:
+    within 1e-12.  A dropped tap, a wrong (ky, kx) decode or a missing bias fails it."""
+    cfg = synthgen.CONFIGS[name].with_batch(N)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = synthgen.make_bias(cfg.F, 77)
+    wd = densify(cfg.F, cfg.C, cfg.K, c.rowptr, c.colidx, c.values)
+    ref = torch.nn.functional.conv2d(torch.from_numpy(L.x).double(), torch.from_numpy(wd).double(),
+                                     torch.from_numpy(b).double(), stride=stride, padding=pad).numpy()
+    rng = np.random.default_rng(11)
+    pts = np.stack([rng.integers(0, s, 500) for s in ref.shape], axis=1)
+    edge = np.array([(n, f, yy, xx) for n in (0, ref.shape[0] - 1) for f in (0, ref.shape[1] - 1)
+                     for yy in (0, ref.shape[2] - 1) for xx in (0, ref.shape[3] - 1)])
+    pts = np.concatenate([pts, edge])
+    v = oracle.conv_points_f64(L.x, cfg.F, cfg.K, stride, pad, c.rowptr, c.colidx, c.values, b, pts)
+    assert v.dtype == np.float64
+    assert np.max(np.abs(v - ref[tuple(pts.T)])) <= 1e-12
+
+
 def test_thread_count_invariance():
     cfg = synthgen.CONFIGS["c1"].with_batch(3)
     L = synthgen.make_layer(cfg)
