@@ -55,6 +55,12 @@ struct DenseArgs {
     int LR, LY, RY, ipb, bpi, rows, pitch, cc, nchunks, nstage, fsets;
     int in_bytes, w_bytes, stage_bytes;
     int xoff; // smem column of image column 0 (the TMA box starts at column -xoff)
+    // ordered stream-K (as kernel_pipe.cu): partial sums of split units, flags, tickets
+    int sk;
+    float2 *sk_part;              // [grid][8 warps][NACC][32 lanes]
+    unsigned long long *sk_flag;  // [grid][8 warps]
+    unsigned *sk_ticket;          // [2]
+    unsigned long long epoch;
 };
 
 template <int S>
@@ -63,6 +69,12 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[DMAXSTAGE], empty_bar[DMAXSTAGE];
     __shared__ int done_cnt[DMAXSTAGE];
+    // this CTA's work, in processing order: [head: unit uh, chunks [0, hj) -> park],
+    // nf whole units, [tail: unit ut, chunks [tj, nchunks) -> resume, then store]
+    struct Sched {
+        int bid, uh, hj, nf, uf0, ut, tj, total;
+    };
+    __shared__ Sched sch;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ns = a.nstage;
     const uint32_t smem0 = smem_u32(smem);
@@ -80,14 +92,45 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
 
     const int nblocks = a.ipb > 1 ? (a.N + a.ipb - 1) / a.ipb : a.N * a.bpi;
     const int nunits = nblocks * a.fsets;
-    const int nmine = int(blockIdx.x) < nunits ? (nunits - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
-    const int total = nmine * a.nchunks;
+    const int nch = a.nchunks;
+    if (threadIdx.x == 0) {
+        Sched q{0, 0, 0, 0, 0, 0, 0, 0};
+        if (a.sk) {
+            // ordered stream-K: the CTA with arrival ticket b owns chunk steps
+            // [b*T/G, (b+1)*T/G) of the unit sequence (see kernel_pipe.cu for why a
+            // ticket rather than blockIdx.x)
+            const int b = int(atomicAdd(a.sk_ticket, 1u));
+            const int64_t T = int64_t(nunits) * nch;
+            const int64_t s0 = T * b / gridDim.x, e0 = T * (b + 1) / gridDim.x;
+            q.bid = b;
+            if (e0 % nch) { q.uh = int(e0 / nch); q.hj = int(e0 % nch); }
+            if (s0 % nch) { q.ut = int(s0 / nch); q.tj = int(s0 % nch); }
+            q.uf0 = int((s0 + nch - 1) / nch);
+            q.nf = int(e0 / nch) - q.uf0;
+            q.total = q.hj + q.nf * nch + (q.tj ? nch - q.tj : 0);
+        } else {
+            q.bid = int(blockIdx.x);
+            q.uf0 = q.bid;
+            q.nf = q.bid < nunits ? (nunits - 1 - q.bid) / int(gridDim.x) + 1 : 0;
+            q.total = q.nf * nch;
+        }
+        sch = q;
+    }
+    __syncthreads();
+    const Sched sc = sch;
+    auto full_unit = [&](int i) { return a.sk ? sc.uf0 + i : sc.uf0 + i * int(gridDim.x); };
 
     // stage kk of this CTA's sequence: the TMA box of its unit's rows x cc channels and
     // the weight slab of its channel set, on the stage's full barrier (one lane)
     auto fill = [&](int kk) {
         const int s = kk % ns;
-        const int u = int(blockIdx.x) + (kk / a.nchunks) * int(gridDim.x), j = kk % a.nchunks;
+        int u, j;
+        if (kk < sc.hj) { u = sc.uh; j = kk; }
+        else {
+            const int k2 = kk - sc.hj;
+            if (k2 < sc.nf * nch) { u = full_unit(k2 / nch); j = k2 % nch; }
+            else { u = sc.ut; j = sc.tj + (k2 - sc.nf * nch); }
+        }
         const int fs = u % a.fsets, blk = u / a.fsets;
         int n, iy;
         if (a.ipb > 1) { n = blk * a.ipb; iy = -1; }
@@ -98,11 +141,11 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(fb, uint32_t(a.ipb * a.cc * a.rows * a.pitch) * 4u + uint32_t(a.w_bytes));
         tma_load_4d(&tmap, fb, dst, -a.xoff, iy, j * a.cc, n);
-        bulk_load(dst + uint32_t(a.in_bytes), a.wslab + (size_t(fs) * a.nchunks + j) * (a.w_bytes / 4),
+        bulk_load(dst + uint32_t(a.in_bytes), a.wslab + (size_t(fs) * nch + j) * (a.w_bytes / 4),
                   uint32_t(a.w_bytes), fb);
     };
     if (threadIdx.x == 0)
-        for (int kk = 0; kk < min(ns, total); ++kk) fill(kk);
+        for (int kk = 0; kk < min(ns, sc.total); ++kk) fill(kk);
 
     // consumer lane -> (image slot, lane row in it, tile column)
     const int lx = lane % a.LR, ly = lane / a.LR;
@@ -112,20 +155,44 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
     // word offset of this thread's window inside a stage's input box
     const int win = lane_ok ? (im * a.cc * a.rows + yl * DT) * a.pitch + S * lx + a.xoff - 1 : 0;
     const int ch_words = a.rows * a.pitch;
+    constexpr int NACC = DR / 2 * DT * S; // float2 accumulators per thread
 
+    const int nitems = (sc.hj > 0) + sc.nf + (sc.tj > 0);
     int kk = 0;
-    for (int i = 0; i < nmine; ++i) {
-        const int u = int(blockIdx.x) + i * int(gridDim.x);
+    for (int it = 0; it < nitems; ++it) {
+        int u, j0 = 0, j1 = nch, kind = 0; // kind: 0 whole unit, 1 head (park), 2 tail (resume)
+        if (sc.hj > 0 && it == 0) { u = sc.uh; j1 = sc.hj; kind = 1; }
+        else {
+            const int i2 = it - (sc.hj > 0);
+            if (i2 < sc.nf) u = full_unit(i2);
+            else { u = sc.ut; j0 = sc.tj; kind = 2; }
+        }
         const int fs = u % a.fsets, blk = u / a.fsets;
         float2 acc[DR / 2][DT][S];
+        if (kind == 2) {
+            // resume: CTA b-1 parked this unit's partial sums (it did that first)
+            const size_t slot = size_t(sc.bid - 1) * DW + warp;
+            unsigned long long f;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a.sk_flag + slot) : "memory");
+            } while (f != a.epoch);
+            const float2 *src = a.sk_part + slot * NACC * 32 + lane;
 #pragma unroll
-        for (int p = 0; p < DR / 2; ++p)
+            for (int p = 0; p < DR / 2; ++p)
 #pragma unroll
-            for (int t = 0; t < DT; ++t)
+                for (int t = 0; t < DT; ++t)
 #pragma unroll
-                for (int q = 0; q < S; ++q) acc[p][t][q] = make_float2(0.0f, 0.0f);
+                    for (int q = 0; q < S; ++q) acc[p][t][q] = __ldcg(src + size_t((p * DT + t) * S + q) * 32);
+        } else {
+#pragma unroll
+            for (int p = 0; p < DR / 2; ++p)
+#pragma unroll
+                for (int t = 0; t < DT; ++t)
+#pragma unroll
+                    for (int q = 0; q < S; ++q) acc[p][t][q] = make_float2(0.0f, 0.0f);
+        }
 
-        for (int j = 0; j < a.nchunks; ++j, ++kk) {
+        for (int j = j0; j < j1; ++j, ++kk) {
             const int s = kk % ns, rnd = kk / ns;
             mbar_wait(smem_u32(&full_bar[s]), uint32_t(rnd & 1));
             const float *in = reinterpret_cast<const float *>(smem + size_t(s) * a.stage_bytes) + win;
@@ -163,9 +230,27 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
                 const int old = atomicAdd(&done_cnt[s], 1);
                 if (old == rnd * DW + DW - 1) {
                     mbar_wait(smem_u32(&empty_bar[s]), uint32_t(rnd & 1)); // acquire every warp's reads
-                    if (kk + ns < total) fill(kk + ns);
+                    if (kk + ns < sc.total) fill(kk + ns);
                 }
             }
+        }
+
+        if (kind == 1) {
+            // park: this warp's partial sums into slot (b, warp) for CTA b+1
+            float2 *dst = a.sk_part + (size_t(sc.bid) * DW + warp) * NACC * 32 + lane;
+#pragma unroll
+            for (int p = 0; p < DR / 2; ++p)
+#pragma unroll
+                for (int t = 0; t < DT; ++t)
+#pragma unroll
+                    for (int q = 0; q < S; ++q) __stcg(dst + size_t((p * DT + t) * S + q) * 32, acc[p][t][q]);
+            __threadfence();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.sk_flag + size_t(sc.bid) * DW + warp),
+                             "l"(a.epoch)
+                             : "memory");
+            continue;
         }
 
         // epilogue: + bias (one FP32 add), store the lane's 2 x S pixels of its 8 channels
@@ -191,6 +276,18 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
                         yp[(size_t)oy * a.Wo + ox] = __fadd_rn(v, b);
                     }
                 }
+            }
+        }
+    }
+    if (a.sk) {
+        // the last CTA to finish resets the arrival counters for the next launch
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(a.sk_ticket + 1, 1u) == gridDim.x - 1) {
+                a.sk_ticket[0] = 0u;
+                a.sk_ticket[1] = 0u;
+                __threadfence();
             }
         }
     }
@@ -242,9 +339,14 @@ int dense_conflicts(const DenseGeometry &g, int pitch) {
 
 } // namespace
 
+bool dense_stream_k(const Plan &p, int64_t nunits, int grid) {
+    if (p.knobs.sk >= 0) return p.knobs.sk == 1 && nunits > grid;
+    return nunits > grid && nunits % grid != 0 && nunits < 16 * int64_t(grid);
+}
+
 bool dense_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     (void)C; (void)H; (void)F;
-    return K == 3 && stride == 1 && pad == 1 && W <= 248;
+    return K == 3 && stride == 1 && pad == 1 && W <= 224; // 32 lanes x 7 columns
 }
 
 void dense_geometry(const Plan &p, DenseGeometry &g) {
@@ -357,6 +459,23 @@ cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStr
         if (xp) cudaFreeAsync(xp, s);
         return cudaErrorInvalidValue;
     }
+    // ordered stream-K when the units do not divide evenly over the persistent CTAs
+    // (c2 shape: 224 units on 148 SMs would leave the second round a third full)
+    a.sk = dense_stream_k(p, nunits, grid) ? 1 : 0;
+    a.sk_part = nullptr; a.sk_flag = nullptr; a.sk_ticket = nullptr; a.epoch = 0;
+    SkWorkspace skws;
+    if (a.sk) {
+        const size_t part_bytes = size_t(grid) * DW * (DR / 2 * DT * g.S) * 32 * sizeof(float2);
+        cudaError_t e = stream_k_workspace(p, s, part_bytes, grid * DW, skws);
+        if (e != cudaSuccess) {
+            if (xp) cudaFreeAsync(xp, s);
+            return e;
+        }
+        a.sk_part = reinterpret_cast<float2 *>(skws.part);
+        a.sk_flag = skws.flag;
+        a.sk_ticket = skws.ticket;
+        a.epoch = next_sk_epoch();
+    }
     cudaError_t err;
     {
         cudaLaunchConfig_t cfg = {};
@@ -376,6 +495,10 @@ cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStr
             err = cudaFuncSetAttribute(dense_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem_bytes));
             if (err == cudaSuccess) err = cudaLaunchKernelEx(&cfg, dense_kernel<8>, map, a);
         }
+    }
+    {
+        cudaError_t e2 = skws.release(s);
+        if (err == cudaSuccess) err = e2;
     }
     if (xp) {
         cudaError_t e2 = cudaFreeAsync(xp, s);

@@ -933,6 +933,82 @@ int sm_count_of_current_device() {
     return sm_count[dev & 63];
 }
 
+unsigned long long next_sk_epoch() {
+    // a tagged, process-unique value: stale workspace contents never equal it
+    static std::atomic<unsigned long long> epochs{0};
+    return 0x5ec0'0000'0000'0000ull | (++epochs & 0x0000'ffff'ffff'ffffull);
+}
+
+cudaError_t SkWorkspace::release(cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (async && base) e = cudaFreeAsync(base, s);
+    base = nullptr;
+    if (lock.owns_lock()) lock.unlock();
+    return e;
+}
+
+// The stream-K workspace of a launch on stream s (pipe and dense kernels): layout
+// [0, 16) arrival ticket + finished-CTA counter (0 between launches), [16, ...) the
+// per-(CTA, warp) u64 flags, parked partial sums from kSkHeader on.  One workspace per
+// (plan, stream), kept and grown (launches on one stream are ordered by
+// griddepcontrol.wait; both kernels leave the counters at 0); the plan's workspace lock
+// is HELD in w until w.release(), so a concurrent call on the same stream cannot
+// replace the buffer between this lookup and its launch.  Under stream capture, or
+// beyond 8 streams, a stream-ordered allocation per call.
+cudaError_t stream_k_workspace(const Plan &p, cudaStream_t s, size_t part_bytes, int nflags, SkWorkspace &w) {
+    const size_t need = kSkHeader + part_bytes;
+    if (16 + size_t(nflags) * 8 > kSkHeader) return cudaErrorInvalidConfiguration;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    bool cached = cap == cudaStreamCaptureStatusNone;
+    Plan &mp = const_cast<Plan &>(p);
+    if (cached) {
+        w.lock = std::unique_lock<std::mutex>(mp.sk_mu);
+        bool known = false;
+        for (auto &x : mp.sk_ws) known |= x.first == s;
+        cached = known || mp.sk_ws.size() < 8;
+        if (!cached) w.lock.unlock();
+    }
+    if (!cached) {
+        keep_pool_cached();
+        cudaError_t e = cudaMallocAsync(&w.base, need, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(w.base, 0, kSkHeader, s);
+        if (e != cudaSuccess) {
+            if (w.base) cudaFreeAsync(w.base, s);
+            w.base = nullptr;
+            return e;
+        }
+        w.async = true;
+    } else {
+        std::pair<void *, size_t> *ws = nullptr;
+        for (auto &x : mp.sk_ws)
+            if (x.first == s) ws = &x.second;
+        if (!ws) {
+            mp.sk_ws.push_back({s, {nullptr, 0}});
+            ws = &mp.sk_ws.back().second;
+        }
+        if (ws->second < need) {
+            if (ws->first) {
+                // the old buffer may still be in use by earlier launches on s
+                cudaStreamSynchronize(s);
+                cudaFree(ws->first);
+                ws->first = nullptr;
+                ws->second = 0;
+            }
+            cudaError_t e = cudaMalloc(&ws->first, need);
+            if (e != cudaSuccess) return e;
+            ws->second = need;
+            cudaMemsetAsync(ws->first, 0, kSkHeader, s); // counters and flags start at 0
+        }
+        w.base = ws->first;
+    }
+    char *b = static_cast<char *>(w.base);
+    w.ticket = reinterpret_cast<unsigned *>(b);
+    w.flag = reinterpret_cast<unsigned long long *>(b + 16);
+    w.part = b + kSkHeader;
+    return cudaSuccess;
+}
+
 // The launch schedule of one forward of N images (staging mode, units, persistent
 // grid, stream-K): the single source of these decisions for launch_pipe and for the
 // spconv_launch_info query the tests assert on.
@@ -1020,8 +1096,6 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     }
     const int grid = sched.grid;
     a.sk = sched.sk ? 1 : 0; a.sk_part = nullptr; a.sk_flag = nullptr; a.sk_ticket = nullptr; a.epoch = 0;
-    std::unique_lock<std::mutex> ws_lock; // the cached stream-K workspace's lock (see below)
-    void *skw = nullptr, *sk_async = nullptr;
     a.trace = nullptr;
     a.rev = p.knobs.rev;
     const bool tracing = p.knobs.trace[0] != 0;
@@ -1032,71 +1106,19 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     if (prof_out[0] && cudaMalloc(&a.prof, 5 * sizeof(unsigned long long)) == cudaSuccess)
         cudaMemsetAsync(a.prof, 0, 5 * sizeof(unsigned long long), s);
 #endif
+    SkWorkspace skws;
     if (a.sk) {
-        static std::atomic<unsigned long long> epochs{0};
         const int qn = p.R * g.T * g.S / 4;
         const size_t part_bytes = size_t(grid) * p.gpc * qn * 32 * sizeof(ulonglong2);
-        // flags [grid][gpc] u64, then 16 bytes: the arrival ticket and finished-CTA counters
-        const size_t flag_bytes = size_t(grid) * p.gpc * sizeof(unsigned long long) + 16;
-        // one workspace per (plan, stream), kept: launches on one stream are ordered
-        // (griddepcontrol.wait), launches on different streams never share one.  Under
-        // stream capture a stream-ordered allocation is used instead (capturable).
-        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-        cudaStreamIsCapturing(s, &cap);
-        bool cached = cap == cudaStreamCaptureStatusNone;
-        Plan &mp = const_cast<Plan &>(p);
-        if (cached) {
-            // held until the launch is enqueued: a concurrent call on the same stream
-            // cannot replace (free) the workspace between our lookup and our launch
-            ws_lock = std::unique_lock<std::mutex>(mp.sk_mu);
-            bool known = false;
-            for (auto &w : mp.sk_ws) known |= w.first == s;
-            cached = known || mp.sk_ws.size() < 8; // at most 8 cached streams per plan (~19 MB each on c2)
-            if (!cached) ws_lock.unlock();
+        cudaError_t e = stream_k_workspace(p, s, part_bytes, grid * p.gpc, skws);
+        if (e != cudaSuccess) {
+            if (xp) cudaFreeAsync(xp, s);
+            return e;
         }
-        if (!cached) {
-            keep_pool_cached();
-            cudaError_t e = cudaMallocAsync(&skw, part_bytes + flag_bytes, s);
-            if (e == cudaSuccess) // the arrival counters start at 0 (flags never equal a fresh epoch)
-                e = cudaMemsetAsync(static_cast<char *>(skw) + part_bytes + flag_bytes - 16, 0, 16, s);
-            if (e != cudaSuccess) {
-                if (skw) cudaFreeAsync(skw, s);
-                if (xp) cudaFreeAsync(xp, s);
-                return e;
-            }
-            sk_async = skw;
-        } else {
-            std::pair<void *, size_t> *ws = nullptr;
-            for (auto &w : mp.sk_ws)
-                if (w.first == s) ws = &w.second;
-            if (!ws) {
-                mp.sk_ws.push_back({s, {nullptr, 0}});
-                ws = &mp.sk_ws.back().second;
-            }
-            if (ws->second < part_bytes + flag_bytes) {
-                if (ws->first) {
-                    // the old buffer may still be in use by earlier launches on s
-                    cudaStreamSynchronize(s);
-                    cudaFree(ws->first);
-                    ws->first = nullptr;
-                    ws->second = 0;
-                }
-                cudaError_t e = cudaMalloc(&ws->first, part_bytes + flag_bytes);
-                if (e != cudaSuccess) {
-                    if (xp) cudaFreeAsync(xp, s);
-                    return e;
-                }
-                ws->second = part_bytes + flag_bytes;
-                // flags and arrival counters start at 0 (flags never equal an epoch)
-                cudaMemsetAsync(static_cast<char *>(ws->first) + part_bytes, 0, flag_bytes, s);
-            }
-            skw = ws->first;
-        }
-        a.sk_part = reinterpret_cast<ulonglong2 *>(skw);
-        a.sk_flag = reinterpret_cast<unsigned long long *>(static_cast<char *>(skw) + part_bytes);
-        a.sk_ticket = reinterpret_cast<unsigned *>(static_cast<char *>(skw) + part_bytes + flag_bytes - 16);
-        // a tagged, process-unique value: stale workspace contents never equal it
-        a.epoch = 0x5ec0'0000'0000'0000ull | (++epochs & 0x0000'ffff'ffff'ffffull);
+        a.sk_part = reinterpret_cast<ulonglong2 *>(skws.part);
+        a.sk_flag = skws.flag;
+        a.sk_ticket = skws.ticket;
+        a.epoch = next_sk_epoch();
     }
     cudaError_t err = cudaErrorInvalidValue;
 #define SPC_PIPE_MODES(RR, TT, SS, FF, DD, EE)                                                           \
@@ -1155,8 +1177,8 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         cudaFree(a.prof);
     }
 #endif
-    if (sk_async) {
-        cudaError_t e2 = cudaFreeAsync(sk_async, s);
+    {
+        cudaError_t e2 = skws.release(s);
         if (err == cudaSuccess) err = e2;
     }
     if (xp) {

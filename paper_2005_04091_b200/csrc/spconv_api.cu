@@ -745,6 +745,7 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
         DeviceGuard guard(p->device);
         if (!guard.ok) return SPCONV_ERR_CUDA;
         info->grid = int(std::min<int64_t>(info->units, spconv::sm_count_of_current_device()));
+        info->stream_k = spconv::dense_stream_k(*p, info->units, info->grid) ? 1 : 0;
         info->staging = (g.padded || (reinterpret_cast<uintptr_t>(x) & 15)) ? 1 : 0;
         info->channels_per_stage = g.cc;
         info->stages = g.nstage;

@@ -165,6 +165,19 @@ struct PipeSchedule {
     int launches = 1;                   // kernel launches per call
 };
 bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q);
+// Stream-K workspace of one launch (kernel_pipe.cu, shared by the dense kernel).
+constexpr size_t kSkHeader = 32768; // ticket + counter, then u64 flags; partial sums after
+struct SkWorkspace {
+    void *base = nullptr;
+    bool async = false;                 // a per-call stream-ordered allocation (freed by release)
+    std::unique_lock<std::mutex> lock;  // the plan's workspace lock, held until release
+    unsigned *ticket = nullptr;
+    unsigned long long *flag = nullptr;
+    void *part = nullptr;
+    cudaError_t release(cudaStream_t s);
+};
+cudaError_t stream_k_workspace(const Plan &p, cudaStream_t s, size_t part_bytes, int nflags, SkWorkspace &w);
+unsigned long long next_sk_epoch();
 int sm_count_of_current_device();
 
 // kernel_pipe.cu
@@ -174,13 +187,16 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
                         bool fused, cudaStream_t s, const float *res = nullptr, int epi = 0);
 
 // kernel_dense.cu.  AUTO routes conv-only calls of layers at or above this density to
-// the dense kernel (the measured B200 break-even, DESIGN.md NEXT-1).
-constexpr double kDenseBreakEven = 0.55;
+// the dense kernel: the measured B200 break-even of the sparse pipe kernel against it is
+// 0.45 (c2 shape), 0.46 (c5), 0.56 (c4) (profiles/r02/breakeven_*.jsonl; DESIGN.md
+// NEXT-1; the paper's own CPU figure is 0.435).
+constexpr double kDenseBreakEven = 0.50;
 bool dense_supported(int C, int H, int W, int F, int K, int stride, int pad);
 void dense_geometry(const Plan &p, DenseGeometry &g);
 std::vector<float> dense_weights(const Plan &p, const DenseGeometry &g, const std::vector<int32_t> &rowptr,
                                  const std::vector<int32_t> &colidx, const std::vector<float> &values);
 cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStream_t s);
+bool dense_stream_k(const Plan &p, int64_t nunits, int grid);
 
 // kernel_tiled.cu
 bool tiled_supported(int C, int H, int W, int F, int K, int stride, int pad);

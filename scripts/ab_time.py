@@ -23,15 +23,22 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def child(cfg_name, density, iters, reps, kernel, rows):
+def child(cfg_name, density, iters, reps, kernel, rows, batch=0):
     import numpy as np
     import torch
 
     import synthgen
     from paper_2005_04091_b200 import spconv
-    cfg = synthgen.CONFIGS[cfg_name]
+    if cfg_name.startswith("custom:"):  # custom:N,C,H,W,F,density (K=3 pad 1)
+        n_, c_, h_, w_, f_, d_ = cfg_name.split(":", 1)[1].split(",")
+        cfg = synthgen.LayerConfig(6, "custom", int(n_), int(c_), int(h_), int(w_), int(f_), 3, 1, 1, float(d_),
+                                   False, False)
+    else:
+        cfg = synthgen.CONFIGS[cfg_name]
     if density:
         cfg = cfg.with_density(density)
+    if batch:
+        cfg = cfg.with_batch(batch)
     L = synthgen.make_layer(cfg)
     layer = spconv.SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, cfg.K, cfg.stride, cfg.pad, L.csr.rowptr,
                                 L.csr.colidx, L.csr.values, L.bias, kernel=kernel, rows_per_group=rows)
@@ -68,6 +75,7 @@ def child(cfg_name, density, iters, reps, kernel, rows):
     ms = statistics.median(res)
     info = layer.info
     out = {"lib": os.environ.get("SPCONV_LIB", "default"), "config": cfg_name, "density": cfg.density,
+           "N": cfg.N, "kernel_req": kernel,
            "us": round(ms * 1e3, 3), "tflops": round(cfg.useful_flops / ms / 1e9, 3),
            "min_us": round(min(res) * 1e3, 3), "R": int(info["rows_per_group"]),
            "kernel": int(info["kernel"]),
@@ -86,25 +94,32 @@ def main():
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--rows", type=int, default=0)
     ap.add_argument("--envs", default="", help="';'-separated env sets, each 'K=V,K=V' (A/B knobs)")
+    ap.add_argument("--batches", default="", help="comma-separated batch overrides")
+    ap.add_argument("--kernels", default="", help="comma-separated kernels to compare (overrides --kernel)")
     ap.add_argument("--child", nargs=2)
+    ap.add_argument("--batch", type=int, default=0)
     args = ap.parse_args()
     if args.child:
-        child(args.child[0], float(args.child[1]), args.iters, args.reps, args.kernel, args.rows)
+        child(args.child[0], float(args.child[1]), args.iters, args.reps, args.kernel, args.rows, args.batch)
         return
     libs = [os.path.abspath(x) for x in args.libs.split(",") if x] or [""]
     envs = [dict(kv.split("=", 1) for kv in e.split(",") if kv) for e in args.envs.split(";")] if args.envs else [{}]
     dens = [float(d) for d in args.densities.split(",") if d] or [0.0]
+    batches = [int(b) for b in args.batches.split(",") if b] or [0]
+    kernels = [k for k in args.kernels.split(",") if k] or [args.kernel]
     for _ in range(args.rounds):
-        for c in args.configs.split(","):
+        for c in args.configs.split(";" if ";" in args.configs or args.configs.startswith("custom:") else ","):
             for d in dens:
-                for lib in libs:
-                    for e in envs:
-                        env = dict(os.environ, **e)
-                        if lib:
-                            env["SPCONV_LIB"] = lib
-                        subprocess.run([sys.executable, __file__, "--child", c, str(d), "--iters", str(args.iters),
-                                        "--reps", str(args.reps), "--kernel", args.kernel, "--rows", str(args.rows)],
-                                       env=env, timeout=600)
+                for bt in batches:
+                    for kern in kernels:
+                        for lib in libs:
+                            for e in envs:
+                                env = dict(os.environ, **e)
+                                if lib:
+                                    env["SPCONV_LIB"] = lib
+                                subprocess.run([sys.executable, __file__, "--child", c, str(d), "--iters",
+                                                str(args.iters), "--reps", str(args.reps), "--kernel", kern,
+                                                "--rows", str(args.rows), "--batch", str(bt)], env=env, timeout=600)
 
 
 if __name__ == "__main__":
