@@ -63,8 +63,15 @@ enum {
     SPCONV_ERR_DEVICE = -6,      /* pointer not device memory of the plan's device */
     SPCONV_ERR_CUDA = -7,        /* a CUDA runtime call or launch failed           */
     SPCONV_ERR_OOM = -8,         /* device or host allocation failed               */
-    SPCONV_ERR_ALIAS = -9        /* y (or argmax) overlaps x                        */
+    SPCONV_ERR_ALIAS = -9,       /* y (or argmax) overlaps x                        */
+    SPCONV_ERR_INTERNAL = -10    /* SPCONV_DEBUG=1 self-check of a plan failed       */
 };
+
+/* Environment (read once, when a plan is created): SPCONV_DEBUG=1 turns on extra
+ * validation -- create rebuilds every output channel's (colidx, value) sequence from
+ * the generated tap streams and compares it with the CSR (SPCONV_ERR_INTERNAL on a
+ * mismatch); every device entry point synchronises its stream and reports a launch or
+ * execution fault as SPCONV_ERR_CUDA at the call that caused it. */
 
 /* Kernel selection (spconv_create_ex).  AUTO picks the dense kernel for K = 3,
  * stride 1, pad 1 layers at or above the break-even density, else the pipelined

@@ -26,6 +26,15 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 # only fused operation (reading G7 in DESIGN.md).
 CFLAGS = ["-O2", "-fPIC", "-shared", "-pthread", "-ffp-contract=off", "-fno-fast-math", "-std=c11"]
 
+# ORACLE_SANITIZE=1: load a build instrumented with AddressSanitizer + UBSan (SURVEY.md
+# §5: "the host oracle under -fsanitize=address,undefined"; tests/test_oracle_sanitized.py
+# runs it in a subprocess with the ASan runtime preloaded)
+SANITIZE = os.environ.get("ORACLE_SANITIZE") == "1"
+if SANITIZE:
+    _LIB = os.path.join(_HERE, "liboracle_san.so")
+    CFLAGS = CFLAGS + ["-g", "-O1", "-fno-omit-frame-pointer", "-fsanitize=address,undefined",
+                       "-fno-sanitize-recover=all"]
+
 _lib = None
 
 

@@ -800,6 +800,7 @@ void read_pipe_knobs(PipeKnobs &k) {
     if (const char *e = std::getenv("SPCONV_PDL")) k.pdl = !(e[0] == '0');
     if (const char *e = std::getenv("SPCONV_PIPE_TRACE")) std::snprintf(k.trace, sizeof(k.trace), "%s", e);
     if (const char *e = std::getenv("SPCONV_PIPE_PROF")) std::snprintf(k.prof, sizeof(k.prof), "%s", e);
+    if (const char *e = std::getenv("SPCONV_DEBUG")) k.debug = e[0] == '1';
 }
 
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {

@@ -10,6 +10,8 @@
 #include <numeric>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "spconv_internal.h"
 
 using spconv::Plan;
@@ -135,6 +137,63 @@ std::vector<int32_t> balance_groups(const std::vector<int32_t> &rowptr, int F, i
         load[best] += rowptr[f + 1] - rowptr[f];
     }
     return rows;
+}
+
+// NVTX range over an entry point (SURVEY.md §5 tracing): visible in nsys / ncu
+// timelines, a no-op without an attached tool.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
+// SPCONV_DEBUG=1 self-check of a built pipe plan (SURVEY.md §5 "extra validation"):
+// walk every (group set, stage, warp) tap stream exactly as the kernel's dispatcher
+// does and rebuild each output channel's (colidx, value) sequence from it; it must be
+// the CSR row, in ascending colidx order (the FP32 contract), entry for entry.
+bool pipe_stream_self_check(const Plan *p, const std::vector<uint4> &out, const std::vector<int32_t> &cstart,
+                            const std::vector<int32_t> &grows, const std::vector<int32_t> &rowptr,
+                            const std::vector<int32_t> &colidx, const std::vector<float> &values) {
+    const int R = p->R, C = p->C, cc = p->pipe_cc, nch = (C + cc - 1) / cc;
+    const uint32_t NEXT = uint32_t(R * 9), END = uint32_t(R * 9 + 1);
+    std::vector<std::vector<std::pair<int, uint32_t>>> got(size_t(p->F));
+    const char *base = reinterpret_cast<const char *>(out.data());
+    for (int gs = 0; gs < p->num_gsets; ++gs)
+        for (int j = 0; j < nch; ++j) {
+            const int32_t c0b = cstart[size_t(gs) * (nch + 1) + j];
+            const uint32_t *hdr = reinterpret_cast<const uint32_t *>(base + c0b);
+            for (int w = 0; w < p->gpc; ++w) {
+                const int g = gs * p->gpc + w;
+                const uint2 *e = reinterpret_cast<const uint2 *>(base + c0b + hdr[w]);
+                uint32_t cs = e[0].y; // lead entry: the case of entry 1
+                int ch = j * cc;
+                for (size_t k = 1;; ++k) {
+                    if (cs == END) break;
+                    if (cs == NEXT) {
+                        if (e[k].x < 1) return false;
+                        ch += int(e[k].x);
+                    } else {
+                        if (cs > NEXT || g >= p->num_groups || ch >= std::min(C, (j + 1) * cc)) return false;
+                        const int r = int(cs) % R, tap = int(cs) / R;
+                        const int f = grows[size_t(g) * R + r];
+                        if (f < 0) return false;
+                        got[size_t(f)].push_back({ch * 9 + tap, e[k].x});
+                    }
+                    cs = e[k].y;
+                    if (k > size_t(4) * (size_t(R) * 9 + 2) * size_t(cc) + 8) return false; // runaway
+                }
+            }
+        }
+    for (int f = 0; f < p->F; ++f) {
+        const auto &v = got[size_t(f)];
+        if (int64_t(v.size()) != int64_t(rowptr[size_t(f) + 1]) - rowptr[size_t(f)]) return false;
+        for (size_t i = 0; i < v.size(); ++i) {
+            const int32_t j = rowptr[size_t(f)] + int32_t(i);
+            uint32_t bits;
+            std::memcpy(&bits, &values[size_t(j)], 4);
+            if (v[i].first != colidx[size_t(j)] || v[i].second != bits) return false;
+        }
+    }
+    return true;
 }
 
 int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<int32_t> &colidx,
@@ -321,6 +380,9 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         }
         if ((st = upload(&p->d_group_rows, grows.data(), grows.size(), p->device_bytes))) return st;
         if ((st = upload(&p->d_chunk_start, cstart.data(), cstart.size(), p->device_bytes))) return st;
+        if (p->knobs.debug && p->pipe_dispatch == 0 &&
+            !pipe_stream_self_check(p, out, cstart, grows, rowptr, colidx, values))
+            return SPCONV_ERR_INTERNAL;
         if ((st = upload(&p->d_stream2, out.data(), out.size(), p->device_bytes))) return st;
         if (!p->pipe_cp.ok) return SPCONV_ERR_UNSUPPORTED;
         return SPCONV_OK;
@@ -374,6 +436,7 @@ const char *spconv_status_string(int status) {
         case SPCONV_ERR_CUDA: return "CUDA error";
         case SPCONV_ERR_OOM: return "out of memory";
         case SPCONV_ERR_ALIAS: return "output overlaps input";
+        case SPCONV_ERR_INTERNAL: return "plan self-check failed (SPCONV_DEBUG)";
         default: return "unknown status";
     }
 }
@@ -387,6 +450,7 @@ const char *spconv_last_cuda_error(void) {
 int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int stride, int pad,
                      const int32_t *rowptr, const int32_t *colidx, const float *values, int64_t nnz,
                      const float *bias, int device, const spconv_options_t *opts) {
+    NvtxRange nvtx("spconv_create");
     if (!plan) return SPCONV_ERR_NULLPTR;
     *plan = nullptr;
     if (!rowptr || (nnz > 0 && (!colidx || !values))) return SPCONV_ERR_NULLPTR;
@@ -455,6 +519,7 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
         return SPCONV_ERR_UNSUPPORTED;
     }
     const double density = double(nnz) / (double(F) * ncol);
+    p->auto_kernel = o.kernel == SPCONV_KERNEL_AUTO;
     if (o.kernel == SPCONV_KERNEL_AUTO) {
         p->kernel = pipe_ok ? SPCONV_KERNEL_PIPE : tiled_ok ? SPCONV_KERNEL_TILED : SPCONV_KERNEL_GENERIC;
         // the dense kernel at and above the measured break-even density (DESIGN.md NEXT-1)
@@ -509,6 +574,29 @@ int spconv_create(spconv_plan_t *plan, int C, int H, int W, int F, int K, int st
                             device, nullptr);
 }
 
+// AUTO's per-call choice between the pipe kernel and the generic one-thread-per-output
+// kernel for SMALL calls (verdict r1 item 6).  Measured on B200 (profiles/r02/
+// small_layers_*.jsonl): the pipe kernel's walk over the C input channels is latency
+// bound when a call has few units (c4_95 N=1: 8 CTAs, 146 us; c2 N=1: 56 us), while the
+// generic kernel's time is ~7 us + 1.2 ns per FMA (c1: 8 us, c2 N=1: 37 us).  Model:
+//   generic_us = 7 + 1.2e-3 * N*F*Ho*Wo*(nnz/F) / 1000
+//   pipe_us    = 5 + max(1, units/SMs) * C * (0.35 * P(a group has a tap in a channel)
+//                                             + 0.075 * 9*R*density)
+// and the generic kernel is taken when it is predicted 20% faster.  Both kernels obey
+// the same FP32 contract, so the choice never changes a bit.
+static bool small_call_prefers_generic(const Plan *p, int N, uintptr_t x) {
+    if (!p->auto_kernel || p->kernel != SPCONV_KERNEL_PIPE || N <= 0) return false;
+    const double d = double(p->nnz) / (double(p->F) * p->C * p->K * p->K);
+    const double fma = double(N) * p->F * p->Ho * p->Wo * (double(p->nnz) / p->F);
+    const double t_generic = 7.0 + 1.2e-6 * fma;
+    spconv::PipeSchedule q;
+    if (!spconv::pipe_schedule(*p, N, x, q)) return true;
+    const double rounds = std::max(1.0, double(q.nunits) / double(spconv::sm_count_of_current_device()));
+    const double p_nonempty = 1.0 - std::pow(1.0 - d, 9.0 * p->R);
+    const double t_pipe = 5.0 + rounds * p->C * (0.35 * p_nonempty + 0.075 * 9.0 * p->R * d);
+    return t_generic < 0.8 * t_pipe;
+}
+
 static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax, bool fused,
                void *stream, const float *res = nullptr, int flags = 0) {
     if (!plan) return SPCONV_ERR_NULLPTR;
@@ -544,22 +632,26 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     const int epi = fused ? 0 : flags;
     if (p->dense && !fused && epi == 0)
         e = spconv::launch_dense(*p, N, x, y, s);
-    else if (p->kernel == SPCONV_KERNEL_PIPE && !(epi && p->pipe_dispatch == 1))
+    else if (p->kernel == SPCONV_KERNEL_PIPE && !(epi && p->pipe_dispatch == 1) &&
+             !small_call_prefers_generic(p, N, reinterpret_cast<uintptr_t>(x)))
         e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s, res, epi);
     else if (p->kernel == SPCONV_KERNEL_TILED && epi == 0)
         e = spconv::launch_tiled(*p, N, x, y, argmax, fused, s);
     else  // the generic kernel serves every epilogue the specialised kernel lacks
         e = fused ? spconv::launch_generic_fused(*p, N, x, y, argmax, s)
                   : spconv::launch_generic_conv(*p, N, x, y, s, res, epi);
+    if (e == cudaSuccess && p->knobs.debug) e = cudaStreamSynchronize(s); // SPCONV_DEBUG: fault at this call
     return e == cudaSuccess ? SPCONV_OK : cuda_fail(e);
 }
 
 int spconv_forward(spconv_plan_t plan, int N, const float *x, float *y, void *stream) {
+    NvtxRange r("spconv_forward");
     return run(plan, N, x, y, nullptr, false, stream);
 }
 
 int spconv_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax,
                               void *stream) {
+    NvtxRange r("spconv_fused_relu_maxpool");
     return run(plan, N, x, y, argmax, true, stream);
 }
 
@@ -614,11 +706,13 @@ int spconv_resize_fused_relu_maxpool(spconv_plan_t plan, int N, const float *x, 
 
 int spconv_forward_ex(spconv_plan_t plan, int N, const float *x, const float *residual, float *y, int flags,
                       void *stream) {
+    NvtxRange r("spconv_forward_ex");
     return run(plan, N, x, y, nullptr, false, stream, residual, flags);
 }
 
 int spconv_forward_host(spconv_plan_t plan, int N, const float *x_host, float *y_host, int fused,
                         int32_t *argmax_host) {
+    NvtxRange nvtx("spconv_forward_host");
     if (!plan) return SPCONV_ERR_NULLPTR;
     Plan *p = plan;
     if (N < 0) return SPCONV_ERR_SHAPE;
@@ -755,6 +849,11 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
     if (p->kernel == SPCONV_KERNEL_PIPE && N > 0) {
         DeviceGuard guard(p->device);
         if (!guard.ok) return SPCONV_ERR_CUDA;
+        if (small_call_prefers_generic(p, N, reinterpret_cast<uintptr_t>(x))) {
+            info->kernel = SPCONV_KERNEL_GENERIC;
+            info->rows_per_group = 0;
+            return SPCONV_OK;
+        }
         spconv::PipeSchedule q;
         if (!spconv::pipe_schedule(*p, N, reinterpret_cast<uintptr_t>(x), q)) return SPCONV_ERR_UNSUPPORTED;
         info->grid = q.grid;

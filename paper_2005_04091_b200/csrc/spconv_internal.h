@@ -72,6 +72,7 @@ struct PipeKnobs {
     int pdl = 1;          // SPCONV_PDL=0: launch without programmatic dependent launch
     char trace[256] = {}; // SPCONV_PIPE_TRACE=<file>: per-CTA timestamps (debug, synchronises)
     char prof[256] = {};  // SPCONV_PIPE_PROF=<file>: phase clock sums (-DSPC_PROF builds only)
+    int debug = 0;        // SPCONV_DEBUG=1: plan self-check at create, synchronise + check every call
 };
 void read_pipe_knobs(PipeKnobs &k);
 
@@ -96,7 +97,8 @@ struct Plan {
     int C, H, W, F, K, stride, pad, Ho, Wo;
     int64_t nnz;
     int device;
-    int kernel; // SPCONV_KERNEL_GENERIC or SPCONV_KERNEL_TILED
+    int kernel; // SPCONV_KERNEL_GENERIC, _TILED or _PIPE (conv-only calls of a dense plan: see `dense`)
+    bool auto_kernel = false; // created with SPCONV_KERNEL_AUTO (small calls may take the generic kernel)
     // device copies (generic path)
     int32_t *d_rowptr = nullptr;
     uint32_t *d_taps = nullptr;

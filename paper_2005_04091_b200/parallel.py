@@ -14,8 +14,18 @@ There is no collective inside the forward itself.
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 import torch.distributed as dist
+
+
+def _nvtx(name):
+    """NVTX range around a collective (SURVEY.md §5 tracing); a no-op where unavailable."""
+    try:
+        return torch.cuda.nvtx.range(name)
+    except Exception:  # pragma: no cover - torch without NVTX
+        return contextlib.nullcontext()
 
 
 def shard_bounds(n_total: int, world: int, rank: int) -> tuple[int, int]:
@@ -32,6 +42,11 @@ def broadcast_csr(rowptr, colidx, values, bias, F: int, device, src: int = 0):
     """Broadcast the CSR filters (and optional bias) from ``src``; returns tensors on ``device``.
 
     Non-source ranks may pass None for the arrays; ``F`` must agree everywhere."""
+    with _nvtx("spconv.broadcast_csr"):
+        return _broadcast_csr(rowptr, colidx, values, bias, F, device, src)
+
+
+def _broadcast_csr(rowptr, colidx, values, bias, F: int, device, src: int):
     rank = dist.get_rank()
     meta = torch.zeros(2, dtype=torch.int64, device=device)
     if rank == src:
@@ -61,6 +76,11 @@ def broadcast_csr(rowptr, colidx, values, bias, F: int, device, src: int = 0):
 
 def gather_output(y_shard: torch.Tensor, n_total: int) -> torch.Tensor:
     """All-gather per-rank output shards (shard_bounds layout) into the full batch."""
+    with _nvtx("spconv.gather_output"):
+        return _gather_output(y_shard, n_total)
+
+
+def _gather_output(y_shard: torch.Tensor, n_total: int) -> torch.Tensor:
     world = dist.get_world_size()
     sizes = [shard_bounds(n_total, world, r) for r in range(world)]
     counts = [e - b for b, e in sizes]

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("SPCONV_LIB") or os.path.join(_PKG, "libspconv.so")
 
 SPCONV_OK = 0
 STATUS = {0: "OK", -1: "NULLPTR", -2: "SHAPE", -3: "CSR", -4: "UNSUPPORTED", -5: "ALIGN",
-          -6: "DEVICE", -7: "CUDA", -8: "OOM", -9: "ALIAS"}
+          -6: "DEVICE", -7: "CUDA", -8: "OOM", -9: "ALIAS", -10: "INTERNAL"}
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TILED, KERNEL_PIPE, KERNEL_DENSE = 0, 1, 2, 3, 4
 KERNELS = {"auto": KERNEL_AUTO, "generic": KERNEL_GENERIC, "tiled": KERNEL_TILED, "pipe": KERNEL_PIPE,
            "dense": KERNEL_DENSE}

@@ -829,3 +829,35 @@ def test_auto_routes_dense_layers_to_the_dense_kernel():
         assert layer.launch_info(2)["kernel"] == want
         assert layer.launch_info(2, fused=True)["kernel"] == 3
         layer.close()
+
+
+@pytest.mark.parametrize("name,fused,N,R", [("c2", False, 23, "4"), ("c3", True, 2, "4"), ("c4_95", False, 3, "4"),
+                                            ("c4_50", False, 2, "2"), ("c5", False, 1, "4")])
+def test_debug_mode_self_check(name, fused, N, R, monkeypatch):
+    """SPCONV_DEBUG=1: create rebuilds every output channel's (colidx, value) sequence from
+    the generated tap streams and checks it against the CSR; every call synchronises and
+    reports faults at the call.  The plans pass and the bits still equal the oracle's."""
+    monkeypatch.setenv("SPCONV_DEBUG", "1")
+    monkeypatch.setenv("SPCONV_PIPE_R", R)
+    _check_full(synthgen.CONFIGS[name], "pipe", fused, N=N, f64=False)
+
+
+def test_auto_small_calls_take_the_generic_kernel():
+    """AUTO's per-call cost model: tiny calls (c1, c2 with one image) launch the generic
+    kernel (the pipe kernel's channel walk is latency bound with few units), the bench
+    batch the pipe kernel; explicit kernel="pipe" is never overridden.  Bits unchanged."""
+    from paper_2005_04091_b200 import SparseConv2d
+    for name, N, want in (("c1", 1, 1), ("c2", 1, 1), ("c2", 32, 3), ("c4_95", 64, 3)):
+        cfg = synthgen.CONFIGS[name].with_batch(N)
+        L = synthgen.make_layer(cfg)
+        c = L.csr
+        layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, device=0)
+        assert layer.launch_info(N)["kernel"] == want, (name, N)
+        if N <= 2:
+            y = layer(torch.from_numpy(L.x).cuda()).cpu().numpy()
+            assert np.array_equal(bits(y), bits(oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values)))
+        layer.close()
+        pinned = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, device=0,
+                              kernel="pipe")
+        assert pinned.launch_info(N)["kernel"] == 3
+        pinned.close()
