@@ -50,7 +50,11 @@ constexpr int DMAXSTAGE = 8;
 
 struct DenseArgs {
     const float *x, *bias, *wslab;
+    const float *res; // residual added before the optional ReLU (epi & 2); may alias y
     float *y;
+    int32_t *argmax;  // fused: first-max flat index per pooled output, or null
+    int epi;          // conv-only epilogue: bit 0 ReLU, bit 1 residual (reading R1)
+    int Po, Qo;
     int N, C, H, W, F, Ho, Wo;
     int LR, LY, RY, ipb, bpi, rows, pitch, cc, nchunks, nstage, fsets;
     int in_bytes, w_bytes, stage_bytes;
@@ -63,7 +67,7 @@ struct DenseArgs {
     unsigned long long epoch;
 };
 
-template <int S>
+template <int S, bool FUSED>
 __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const DenseArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -88,7 +92,6 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
     }
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     const int nblocks = a.ipb > 1 ? (a.N + a.ipb - 1) / a.ipb : a.N * a.bpi;
     const int nunits = nblocks * a.fsets;
@@ -117,6 +120,9 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
         sch = q;
     }
     __syncthreads();
+    // the ticket above comes from this launch's own counter slot; x and the parked
+    // partials may only be read once the previous grid is complete
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const Sched sc = sch;
     auto full_unit = [&](int i) { return a.sk ? sc.uf0 + i : sc.uf0 + i * int(gridDim.x); };
 
@@ -253,28 +259,79 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
             continue;
         }
 
-        // epilogue: + bias (one FP32 add), store the lane's 2 x S pixels of its 8 channels
+        // epilogue (a6): + bias (one FP32 add); conv: [+ residual] [ReLU] and store the
+        // lane's 2 x S pixels of its 8 channels; fused: ReLU, 2x2 max, first-max argmax
         int n, oy0;
         if (a.ipb > 1) { n = blk * a.ipb + im; oy0 = yl * DT; }
         else { n = blk / a.bpi; oy0 = (blk % a.bpi) * a.LY * DT + yl * DT; }
-        if (!lane_ok || n >= a.N) continue;
+        const bool out_ok = lane_ok && n < a.N;
+        if constexpr (!FUSED) {
+            if (!out_ok) continue;
 #pragma unroll
-        for (int r = 0; r < DR; ++r) {
-            const int f = fs * (DW * DR) + warp * DR + r;
-            if (f >= a.F) continue;
-            const float b = __ldg(a.bias + f);
-            float *yp = a.y + ((size_t)n * a.F + f) * a.Ho * a.Wo;
+            for (int r = 0; r < DR; ++r) {
+                const int f = fs * (DW * DR) + warp * DR + r;
+                if (f >= a.F) continue;
+                const float b = __ldg(a.bias + f);
+                const size_t plane = ((size_t)n * a.F + f) * a.Ho * a.Wo;
+                float *yp = a.y + plane;
 #pragma unroll
-            for (int t = 0; t < DT; ++t) {
-                const int oy = oy0 + t;
-                if (oy >= a.Ho) continue;
+                for (int t = 0; t < DT; ++t) {
+                    const int oy = oy0 + t;
+                    if (oy >= a.Ho) continue;
 #pragma unroll
-                for (int q = 0; q < S; ++q) {
-                    const int ox = S * lx + q;
-                    if (ox < a.Wo) {
-                        const float v = (r & 1) ? acc[r / 2][t][q].y : acc[r / 2][t][q].x;
-                        yp[(size_t)oy * a.Wo + ox] = __fadd_rn(v, b);
+                    for (int q = 0; q < S; ++q) {
+                        const int ox = S * lx + q;
+                        if (ox < a.Wo) {
+                            float v = __fadd_rn((r & 1) ? acc[r / 2][t][q].y : acc[r / 2][t][q].x, b);
+                            if (a.epi & 2) v = __fadd_rn(v, a.res[plane + (size_t)oy * a.Wo + ox]);
+                            if (a.epi & 1) v = v > 0.0f ? v : 0.0f;
+                            yp[(size_t)oy * a.Wo + ox] = v;
+                        }
                     }
+                }
+            }
+        } else {
+            // the lane's two rows are one pool row (oy0 is even); its columns S*lx ..
+            // S*lx + S-1.  With S odd, a lane starting on an even column owns the pair
+            // straddling into lane + 1 (whose first column arrives by shuffle); a lane
+            // starting on an odd column leaves its first column to lane - 1.
+            const int py = oy0 >> 1;
+#pragma unroll
+            for (int r = 0; r < DR; ++r) {
+                const int f = fs * (DW * DR) + warp * DR + r;
+                const float b = __ldg(a.bias + min(f, a.F - 1));
+                float rl[DT][S + 1];
+#pragma unroll
+                for (int t = 0; t < DT; ++t) {
+#pragma unroll
+                    for (int q = 0; q < S; ++q) {
+                        const float v = __fadd_rn((r & 1) ? acc[r / 2][t][q].y : acc[r / 2][t][q].x, b);
+                        rl[t][q] = v > 0.0f ? v : 0.0f;
+                    }
+                    rl[t][S] = __shfl_down_sync(0xffffffffu, rl[t][0], 1);
+                }
+                if (!out_ok || f >= a.F || py >= a.Po) continue;
+                float *yp = a.y + ((size_t)n * a.F + f) * a.Po * a.Qo + (size_t)py * a.Qo;
+                int32_t *ap = a.argmax ? a.argmax + ((size_t)n * a.F + f) * a.Po * a.Qo + (size_t)py * a.Qo : nullptr;
+                const int c0 = S * lx;
+#pragma unroll
+                for (int q0 = 0; q0 < S; ++q0) {
+                    if (((c0 + q0) & 1) != 0) continue; // pools start on even columns
+                    const int px = (c0 + q0) >> 1;
+                    if (px >= a.Qo) continue;
+                    float best = 0.0f;
+                    int bidx = 0;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int dy = w >> 1, dx = w & 1;
+                        const float rv = rl[dy][q0 + dx];
+                        if (w == 0 || rv > best) {
+                            best = rv;
+                            bidx = (oy0 + dy) * a.Wo + c0 + q0 + dx;
+                        }
+                    }
+                    yp[px] = best;
+                    if (ap) ap[px] = bidx;
                 }
             }
         }
@@ -417,7 +474,8 @@ std::vector<float> dense_weights(const Plan &p, const DenseGeometry &g, const st
     return w;
 }
 
-cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStream_t s) {
+cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
+                         cudaStream_t s, const float *res, int epi) {
     const DenseGeometry &g = p.dense_geo;
     if (!g.ok || !p.d_wdense || dense_encode() == nullptr) return cudaErrorInvalidConfiguration;
     float *xp = nullptr;
@@ -438,6 +496,7 @@ cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStr
     }
     DenseArgs a;
     a.x = src; a.bias = p.d_bias; a.wslab = p.d_wdense; a.y = y;
+    a.res = res; a.argmax = argmax; a.epi = fused ? 0 : epi; a.Po = p.Ho / 2; a.Qo = p.Wo / 2;
     a.N = N; a.C = p.C; a.H = p.H; a.W = p.W; a.F = p.F; a.Ho = p.Ho; a.Wo = p.Wo;
     a.LR = g.LR; a.LY = g.LY; a.RY = g.RY; a.ipb = g.ipb; a.bpi = g.bpi; a.rows = g.rows; a.pitch = g.pitch;
     a.cc = g.cc; a.nchunks = g.nchunks; a.nstage = g.nstage; a.fsets = g.fsets;
@@ -488,13 +547,12 @@ cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStr
         attr[0].val.programmaticStreamSerializationAllowed = p.knobs.pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (g.S == 7) {
-            err = cudaFuncSetAttribute(dense_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem_bytes));
-            if (err == cudaSuccess) err = cudaLaunchKernelEx(&cfg, dense_kernel<7>, map, a);
-        } else {
-            err = cudaFuncSetAttribute(dense_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem_bytes));
-            if (err == cudaSuccess) err = cudaLaunchKernelEx(&cfg, dense_kernel<8>, map, a);
-        }
+        auto go = [&](auto kern) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem_bytes));
+            return e == cudaSuccess ? cudaLaunchKernelEx(&cfg, kern, map, a) : e;
+        };
+        if (g.S == 7) err = fused ? go(dense_kernel<7, true>) : go(dense_kernel<7, false>);
+        else err = fused ? go(dense_kernel<8, true>) : go(dense_kernel<8, false>);
     }
     {
         cudaError_t e2 = skws.release(s);

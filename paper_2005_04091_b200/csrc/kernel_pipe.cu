@@ -330,23 +330,21 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     }
     __syncthreads();
     // Programmatic dependent launch: let the next launch on the stream start its
-    // prologue on SMs this grid frees, and wait here for the previous grid (whose
-    // outputs x may be, and whose stream-K workspace this launch reuses) to finish.
-    // Without the launch attribute both are no-ops.  Only plan tables (immutable)
-    // were read above.
+    // prologue on SMs this grid frees; griddepcontrol.wait (below, after the schedule)
+    // waits for the previous grid.  Without the launch attribute both are no-ops.
+    // Only plan tables (immutable) and this launch's counter slot are touched before.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     struct Sched {
         int hA, uh, tc0, tC, ut, nf, uf0, hc, tcs, total;
     };
     __shared__ Sched sch;
     __shared__ int s_bid;
     if (threadIdx.x == 0) {
-        // work index.  Stream-K: an arrival ticket (taken after griddepcontrol.wait, so
-        // the previous launch on this workspace has finished and reset the counter):
-        // CTA b's tail waits only for the head of ticket b-1, whose CTA is already
-        // running, so the wait cannot depend on a CTA that is not resident (forward
-        // progress under MPS, green contexts or concurrent kernels).
+        // work index.  Stream-K: an arrival ticket from this launch's counter slot
+        // (stream_k_workspace: never shared with the launch this one overlaps, so it
+        // can be taken before griddepcontrol.wait): CTA b's tail waits only for the
+        // head of ticket b-1, whose CTA is already running, so the wait cannot depend
+        // on a CTA that is not resident (MPS, green contexts, concurrent kernels).
         const int t = a.sk ? int(atomicAdd(a.sk_ticket, 1u)) : int(blockIdx.x);
         const int bid = a.rev ? int(gridDim.x) - 1 - t : t;
         s_bid = bid;
@@ -367,6 +365,9 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         sch = q;
     }
     __syncthreads();
+    // the previous grid (whose outputs x may be, and whose stream-K workspace this
+    // launch reuses) must be complete before x or the parked partials are read
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int bid = s_bid;
     const int &hA = sch.hA, &uh = sch.uh, &tc0 = sch.tc0, &tC = sch.tC, &ut = sch.ut, &nf = sch.nf,
               &uf0 = sch.uf0, &hc = sch.hc, &tcs = sch.tcs, &total = sch.total;
@@ -949,16 +950,18 @@ cudaError_t SkWorkspace::release(cudaStream_t s) {
 }
 
 // The stream-K workspace of a launch on stream s (pipe and dense kernels): layout
-// [0, 16) arrival ticket + finished-CTA counter (0 between launches), [16, ...) the
-// per-(CTA, warp) u64 flags, parked partial sums from kSkHeader on.  One workspace per
-// (plan, stream), kept and grown (launches on one stream are ordered by
-// griddepcontrol.wait; both kernels leave the counters at 0); the plan's workspace lock
-// is HELD in w until w.release(), so a concurrent call on the same stream cannot
-// replace the buffer between this lookup and its launch.  Under stream capture, or
-// beyond 8 streams, a stream-ordered allocation per call.
+// [0, 512) 64 counter slots {arrival ticket, finished CTAs} (0 when unused), [512, ...)
+// one u64 flag per (CTA, warp), parked partial sums from kSkHeader on.  Launch k on a
+// workspace uses counter slot k % 64 -- consecutive launches on a stream (which overlap
+// under programmatic dependent launch) never share a slot, and each launch's last CTA
+// to finish zeroes its slot -- so a CTA can take its ticket BEFORE griddepcontrol.wait.
+// One workspace per (plan, stream), kept and grown; the plan's workspace lock is HELD
+// in w until w.release(), so a concurrent call on the same stream cannot replace the
+// buffer between this lookup and its launch.  Under stream capture, or beyond 8
+// streams, a stream-ordered (zeroed) allocation per call.
 cudaError_t stream_k_workspace(const Plan &p, cudaStream_t s, size_t part_bytes, int nflags, SkWorkspace &w) {
     const size_t need = kSkHeader + part_bytes;
-    if (16 + size_t(nflags) * 8 > kSkHeader) return cudaErrorInvalidConfiguration;
+    if (kSkFlags + size_t(nflags) * 8 > kSkHeader) return cudaErrorInvalidConfiguration;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cap);
     bool cached = cap == cudaStreamCaptureStatusNone;
@@ -966,10 +969,11 @@ cudaError_t stream_k_workspace(const Plan &p, cudaStream_t s, size_t part_bytes,
     if (cached) {
         w.lock = std::unique_lock<std::mutex>(mp.sk_mu);
         bool known = false;
-        for (auto &x : mp.sk_ws) known |= x.first == s;
+        for (auto &x : mp.sk_ws) known |= x.stream == s;
         cached = known || mp.sk_ws.size() < 8;
         if (!cached) w.lock.unlock();
     }
+    unsigned slot = 0;
     if (!cached) {
         keep_pool_cached();
         cudaError_t e = cudaMallocAsync(&w.base, need, s);
@@ -981,31 +985,33 @@ cudaError_t stream_k_workspace(const Plan &p, cudaStream_t s, size_t part_bytes,
         }
         w.async = true;
     } else {
-        std::pair<void *, size_t> *ws = nullptr;
+        Plan::SkSlot *ws = nullptr;
         for (auto &x : mp.sk_ws)
-            if (x.first == s) ws = &x.second;
+            if (x.stream == s) ws = &x;
         if (!ws) {
-            mp.sk_ws.push_back({s, {nullptr, 0}});
-            ws = &mp.sk_ws.back().second;
+            mp.sk_ws.push_back(Plan::SkSlot{s, nullptr, 0, 0});
+            ws = &mp.sk_ws.back();
         }
-        if (ws->second < need) {
-            if (ws->first) {
+        if (ws->bytes < need) {
+            if (ws->ptr) {
                 // the old buffer may still be in use by earlier launches on s
                 cudaStreamSynchronize(s);
-                cudaFree(ws->first);
-                ws->first = nullptr;
-                ws->second = 0;
+                cudaFree(ws->ptr);
+                ws->ptr = nullptr;
+                ws->bytes = 0;
             }
-            cudaError_t e = cudaMalloc(&ws->first, need);
+            cudaError_t e = cudaMalloc(&ws->ptr, need);
             if (e != cudaSuccess) return e;
-            ws->second = need;
-            cudaMemsetAsync(ws->first, 0, kSkHeader, s); // counters and flags start at 0
+            ws->bytes = need;
+            ws->seq = 0;
+            cudaMemsetAsync(ws->ptr, 0, kSkHeader, s); // counters and flags start at 0
         }
-        w.base = ws->first;
+        w.base = ws->ptr;
+        slot = ws->seq++ % unsigned(kSkSlots);
     }
     char *b = static_cast<char *>(w.base);
-    w.ticket = reinterpret_cast<unsigned *>(b);
-    w.flag = reinterpret_cast<unsigned long long *>(b + 16);
+    w.ticket = reinterpret_cast<unsigned *>(b) + 2 * slot;
+    w.flag = reinterpret_cast<unsigned long long *>(b + kSkFlags);
     w.part = b + kSkHeader;
     return cudaSuccess;
 }

@@ -85,7 +85,7 @@ void free_plan(Plan *p) {
     cudaFree(p->d_chunk_start);
     cudaFree(p->d_stream2);
     cudaFree(p->d_wdense);
-    for (auto &w : p->sk_ws) cudaFree(w.second.first);
+    for (auto &w : p->sk_ws) cudaFree(w.ptr);
     cudaFree(p->d_xbuf);
     cudaFree(p->d_ybuf);
     cudaFree(p->d_abuf);
@@ -630,8 +630,8 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e;
     const int epi = fused ? 0 : flags;
-    if (p->dense && !fused && epi == 0)
-        e = spconv::launch_dense(*p, N, x, y, s);
+    if (p->dense)
+        e = spconv::launch_dense(*p, N, x, y, argmax, fused, s, res, epi);
     else if (p->kernel == SPCONV_KERNEL_PIPE && !(epi && p->pipe_dispatch == 1) &&
              !small_call_prefers_generic(p, N, reinterpret_cast<uintptr_t>(x)))
         e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s, res, epi);
@@ -830,7 +830,7 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
     info->rows_per_group = p->R;
     info->launches = N > 0 ? 1 : 0;
     (void)fused;
-    if (p->dense && !fused && N > 0) {
+    if (p->dense && N > 0) {
         const spconv::DenseGeometry &g = p->dense_geo;
         info->kernel = SPCONV_KERNEL_DENSE;
         info->rows_per_group = 8;

@@ -135,7 +135,13 @@ struct Plan {
     // stream-K workspaces of the pipe kernel, one per stream (kept across calls so
     // consecutive launches are adjacent in the stream: programmatic dependent launch)
     std::mutex sk_mu;
-    std::vector<std::pair<cudaStream_t, std::pair<void *, size_t>>> sk_ws;
+    struct SkSlot {
+        cudaStream_t stream = nullptr;
+        void *ptr = nullptr;
+        size_t bytes = 0;
+        unsigned seq = 0; // launches on this workspace: the counter slot of launch k is k % kSkSlots
+    };
+    std::vector<SkSlot> sk_ws;
     cudaStream_t host_stream = nullptr;    // host -> device copies
     static constexpr int HOST_KSTREAMS = 3;
     cudaStream_t host_kstream[HOST_KSTREAMS] = {}; // forwards of spconv_forward_host (chunks round-robin)
@@ -168,7 +174,9 @@ struct PipeSchedule {
 };
 bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q);
 // Stream-K workspace of one launch (kernel_pipe.cu, shared by the dense kernel).
-constexpr size_t kSkHeader = 32768; // ticket + counter, then u64 flags; partial sums after
+constexpr size_t kSkHeader = 32768; // counter slots, then u64 flags; partial sums after
+constexpr int kSkSlots = 64;         // [ticket, finished] pairs, one per launch modulo 64
+constexpr size_t kSkFlags = kSkSlots * 8; // byte offset of the flags
 struct SkWorkspace {
     void *base = nullptr;
     bool async = false;                 // a per-call stream-ordered allocation (freed by release)
@@ -192,12 +200,13 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
 // the dense kernel: the measured B200 break-even of the sparse pipe kernel against it is
 // 0.45 (c2 shape), 0.46 (c5), 0.56 (c4) (profiles/r02/breakeven_*.jsonl; DESIGN.md
 // NEXT-1; the paper's own CPU figure is 0.435).
-constexpr double kDenseBreakEven = 0.50;
+constexpr double kDenseBreakEven = 0.55;
 bool dense_supported(int C, int H, int W, int F, int K, int stride, int pad);
 void dense_geometry(const Plan &p, DenseGeometry &g);
 std::vector<float> dense_weights(const Plan &p, const DenseGeometry &g, const std::vector<int32_t> &rowptr,
                                  const std::vector<int32_t> &colidx, const std::vector<float> &values);
-cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, cudaStream_t s);
+cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
+                         cudaStream_t s, const float *res = nullptr, int epi = 0);
 bool dense_stream_k(const Plan &p, int64_t nunits, int grid);
 
 // kernel_tiled.cu

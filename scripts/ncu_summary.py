@@ -87,6 +87,40 @@ def summarise(rep: str, flops: float | None):
     return res
 
 
+def executed_fmas(rep: str):
+    """Thread-level FMAs the kernel executed, from the SASS source page: every FFMA
+    counts 1 per thread, every packed FFMA2 2 (SURVEY.md §8(d) FFMA efficiency =
+    useful FMAs / executed FMAs).  Also the share of warp-stall samples on the FFMA /
+    FFMA2 instructions."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = next((r for r in rows if "Source" in r and "Thread Instructions Executed" in r), None)
+    if hdr is None:
+        return None
+    i_src, i_thr = hdr.index("Source"), hdr.index("Thread Instructions Executed")
+    i_smp = hdr.index("Warp Stall Sampling (All Samples)") if "Warp Stall Sampling (All Samples)" in hdr else None
+    fma = 0.0
+    smp_all = smp_fma = 0.0
+    for r in rows[rows.index(hdr) + 1:]:
+        if len(r) <= i_thr:
+            continue
+        op = r[i_src].split()
+        if not op:
+            continue
+        opc = op[1] if op[0].startswith("@") and len(op) > 1 else op[0]
+        n = num(r[i_thr]) or 0.0
+        smp = num(r[i_smp]) or 0.0 if i_smp is not None else 0.0
+        smp_all += smp
+        if opc.startswith("FFMA2"):
+            fma += 2 * n
+            smp_fma += smp
+        elif opc.startswith("FFMA"):
+            fma += n
+            smp_fma += smp
+    return {"executed_fmas": fma, "ffma_stall_sample_share": smp_fma / smp_all if smp_all else None}
+
+
 def launches(path: str):
     rows = []
     with open(path) as f:
@@ -114,6 +148,12 @@ def main():
     ap.add_argument("--kernel-name", default="pipe", help="library kernel name recorded with the traffic")
     a = ap.parse_args()
     s = {"report": a.report, "config": a.config, "kernels": summarise(a.report, a.flops)}
+    if a.flops:
+        ex = executed_fmas(a.report)
+        if ex and ex["executed_fmas"]:
+            ex["useful_fmas"] = a.flops / 2
+            ex["ffma_efficiency"] = ex["useful_fmas"] / ex["executed_fmas"]
+            s["ffma"] = ex
     if a.launches:
         s["launch_list"] = launches(a.launches)
     with open(a.out + ".json", "w") as f:
@@ -131,6 +171,10 @@ def main():
             f.write("  top stall reasons (warps per issue-active cycle):\n")
             for k, v in e["stalls_per_issue"].items():
                 f.write(f"    {k:40s} {v}\n")
+        if "ffma" in s:
+            x = s["ffma"]
+            f.write(f"\nFFMA efficiency (useful FMAs / executed thread FMAs, FFMA2 = 2): "
+                    f"{x['useful_fmas']:.4g} / {x['executed_fmas']:.4g} = {x['ffma_efficiency']:.3f}\n")
         if "launch_list" in s:
             f.write("\nlaunch list (ncu gpu__time_duration.sum, --clock-control none):\n")
             for k, v in s["launch_list"].items():

@@ -17,7 +17,7 @@ from tests._util import allclose_contract, bits
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-KERNELS = ["pipe", "tiled", "generic"]
+KERNELS = ["pipe", "tiled", "generic", "dense"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -596,7 +596,7 @@ def test_random_shapes_bitwise_vs_oracle():
         ref = oracle.conv_f32(xh, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b)
         fused_ref = oracle.fused_f32(xh, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b) if H >= 2 and W >= 2 else None
         x = torch.from_numpy(xh).cuda()
-        for kernel in ("auto", "pipe", "tiled"):
+        for kernel in ("auto", "pipe", "tiled", "dense"):
             try:
                 layer = SparseConv2d(C, H, W, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b, kernel=kernel)
             except SpconvError as e:
@@ -816,18 +816,18 @@ def test_dense_kernel_random_shapes():
 
 
 def test_auto_routes_dense_layers_to_the_dense_kernel():
-    """AUTO: conv-only calls of layers at or above the measured break-even density run the
-    dense kernel (plan and launch info say so), sparser layers the pipe kernel."""
-    from paper_2005_04091_b200 import spconv
+    """AUTO: calls on layers at or above the measured break-even density (0.55) run the
+    dense kernel -- conv, fused and block epilogues -- (plan and launch info say so),
+    sparser layers the pipe kernel."""
     from paper_2005_04091_b200.spconv import SparseConv2d
-    for d, want in ((1.0, 4), (0.2, 3)):
-        cfg = synthgen.CONFIGS["c2"].with_density(d).with_batch(2)
-        L = synthgen.make_layer(cfg)
+    for d, want in ((1.0, 4), (0.6, 4), (0.5, 3), (0.2, 3)):
+        cfg = synthgen.CONFIGS["c2"].with_density(d)
+        L = synthgen.make_layer(cfg, with_input=False)
         layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, L.csr.rowptr, L.csr.colidx, L.csr.values,
                              device=0)
-        assert layer.info["kernel"] == want
-        assert layer.launch_info(2)["kernel"] == want
-        assert layer.launch_info(2, fused=True)["kernel"] == 3
+        assert layer.info["kernel"] == want, d
+        assert layer.launch_info(32)["kernel"] == want, d
+        assert layer.launch_info(32, fused=True)["kernel"] == want, d
         layer.close()
 
 
