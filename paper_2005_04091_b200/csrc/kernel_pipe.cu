@@ -64,6 +64,7 @@ struct PipeArgs {
     int xs, tiles_x, tiles_y, ipb, tr, lanes, blocks_y, rs, pitch, nstage, in_words, in_pad, st_bytes;
     int cc, nchunks;
     int band; // 1: the ipb slots of a unit are tile-row bands of the flattened (image, tile row) sequence
+    uint32_t lane_map[32]; // per lane: slot << 16 | tile row << 8 | tile column (lane_tile on the host)
     int gpc, num_groups, num_gsets;
     int tma;
     int ent; // == 8, the tap-stream entry stride: a runtime value so ptxas cannot fold it (SPC2_ENT_REG)
@@ -83,6 +84,27 @@ struct PipeArgs {
 };
 
 using namespace dev; // mbarrier / TMA / bulk-copy wrappers (async_copy.cuh)
+
+// Lane -> (image / band slot, tile row in it, tile column).  order 0: slot-major;
+// order 1: tile-row-major (small images, several per unit: the lanes of a quarter-warp
+// then span two slots, whose offset the pitch search can place on the other half of
+// the shared-memory banks).  The column is always fastest, so lane + 1 is the next
+// tile of the same row (the fused epilogue's shuffle relies on it).
+inline void lane_tile(int li, int order, int ipb, int tr, int tiles_x, int &im, int &tyl, int &tx) {
+    if (order == 0) {
+        const int per_img = tr * tiles_x;
+        im = li / per_img;
+        const int rem = li - im * per_img;
+        tyl = rem / tiles_x;
+        tx = rem - tyl * tiles_x;
+    } else {
+        const int per_row = ipb * tiles_x;
+        tyl = li / per_row;
+        const int rem = li - tyl * per_row;
+        im = rem / tiles_x;
+        tx = rem - im * tiles_x;
+    }
+}
 
 __device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float(uint32_t(v)); }
 __device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(uint32_t(v >> 32)); }
@@ -394,12 +416,10 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         }
     }
 
-    const int per_img_tiles = a.tr * a.tiles_x;
     const bool lane_ok = lane < a.lanes;
-    const int li = lane_ok ? lane : 0;
-    const int im = li / per_img_tiles;
-    const int rem = li - im * per_img_tiles;
-    const int tyl = rem / a.tiles_x, tx = rem - tyl * a.tiles_x;
+    // (slot, tile row, tile column) of this lane, decomposed on the host (lane_tile)
+    const uint32_t lm = a.lane_map[lane_ok ? lane : 0];
+    const int im = int(lm >> 16), tyl = int((lm >> 8) & 0xff), tx = int(lm & 0xff);
     // byte offset of this thread's window inside a stage (16-byte aligned)
     const uint32_t win_off = uint32_t((im * a.cc * a.rs + tyl * PT) * a.pitch + tx * PS) * 4u;
     const uint32_t row_bytes = uint32_t(a.pitch) * 4u;
@@ -757,11 +777,10 @@ cudaError_t launch_one(const CUtensorMap &map, const PipeArgs &a, int grid, size
 int window_wavefronts(const PipeGeometry &g, int pitch) {
     const int PT = g.T, PS = g.S;
     int addr[32];
-    const int per_img = g.tr * g.tiles_x;
     for (int l = 0; l < 32; ++l) {
         const int li = l < g.lanes ? l : 0;
-        const int im = li / per_img, rem = li % per_img;
-        const int tyl = rem / g.tiles_x, tx = rem % g.tiles_x;
+        int im, tyl, tx;
+        lane_tile(li, g.lane_order, g.ipb, g.tr, g.tiles_x, im, tyl, tx);
         addr[l] = (im * g.cc * g.rs + tyl * PT) * pitch + tx * PS; // words (slot im of the stage)
     }
     int total = 0;
@@ -854,20 +873,30 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
     g.cc = p.pipe_cc;
     // smem columns read: window of the last tile ends at 4*(tiles_x-1) + 5
     const int need = ((PS * g.tiles_x + 2) + 3) & ~3;
-    int best = need, best_wf = 1 << 30;
-    for (int cand = need; cand <= need + 32; cand += 4) {
-        // band mode stages every band with its own TMA box into slot b of the stage:
-        // slots must start on 128-byte boundaries (the tensor-copy destination
-        // alignment), i.e. cc * rs * pitch words must be a multiple of 32 (a pitch
-        // multiple of 16 words always qualifies, and the range holds two)
-        if (g.band && (g.cc * g.rs * cand) % 32 != 0) continue;
-        const int wf = window_wavefronts(g, cand);
-        if (wf < best_wf) {
-            best_wf = wf;
-            best = cand;
+    int best = need, best_wf = 1 << 30, best_order = 0;
+    // the lane order matters only with several images AND several tile rows per unit
+    // (c4: 4 images x 2 tile rows: the pitch alone cannot separate the quarter-warp's
+    // two tile rows, 8*pitch = 0 mod 32 words; the image slots can be: 12 -> 8
+    // wavefronts per window row)
+    const int orders = (g.ipb > 1 && g.tr > 1) ? 2 : 1;
+    for (int order = 0; order < orders; ++order) {
+        g.lane_order = order;
+        for (int cand = need; cand <= need + 32; cand += 4) {
+            // band mode stages every band with its own TMA box into slot b of the stage:
+            // slots must start on 128-byte boundaries (the tensor-copy destination
+            // alignment), i.e. cc * rs * pitch words must be a multiple of 32 (a pitch
+            // multiple of 16 words always qualifies, and the range holds two)
+            if (g.band && (g.cc * g.rs * cand) % 32 != 0) continue;
+            const int wf = window_wavefronts(g, cand);
+            if (wf < best_wf) {
+                best_wf = wf;
+                best = cand;
+                best_order = order;
+            }
         }
     }
     g.pitch = best;
+    g.lane_order = best_order;
     if (g.band && (g.cc * g.rs * g.pitch) % 32 != 0) return; // (unreachable: see the search)
     if (tma && (g.pitch > 256 || g.rs > 256)) return;
     if (mode == 0 && (p.W * 4) % 16 != 0) return;
@@ -1079,6 +1108,11 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.lanes = g.lanes; a.blocks_y = g.blocks_y; a.rs = g.rs; a.pitch = g.pitch; a.nstage = g.nstage;
     a.in_words = g.in_words; a.in_pad = g.in_pad; a.st_bytes = g.st_bytes;
     a.cc = g.cc; a.nchunks = g.nchunks; a.band = g.band;
+    for (int l = 0; l < 32; ++l) {
+        int im, tyl, tx;
+        lane_tile(l < g.lanes ? l : 0, g.lane_order, g.ipb, g.tr, g.tiles_x, im, tyl, tx);
+        a.lane_map[l] = (uint32_t(im) << 16) | (uint32_t(tyl) << 8) | uint32_t(tx);
+    }
     a.gpc = p.gpc; a.num_groups = p.num_groups; a.num_gsets = p.num_gsets;
     a.tma = mode != 2 ? 1 : 0;
     a.ent = 8;

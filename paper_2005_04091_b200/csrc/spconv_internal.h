@@ -51,6 +51,7 @@ struct PipeGeometry {
     int tiles_x, tiles_y;    // 4x4 thread tiles per image row / column
     int ipb, tr;             // images (band: tile-row bands) per block, tile rows per block (per image)
     int band;                // 1: blocks are ipb one-tile-row bands of the flattened (image, tile row) sequence
+    int lane_order = 0;      // lane -> tile: 0 slot-major, 1 tile-row-major (kernel_pipe.cu lane_tile)
     int lanes;               // active lanes per consumer warp = ipb * tr * tiles_x
     int blocks_y;            // blocks per image (ipb == 1) along the tile rows
     int rs;                  // staged input rows per image = 4 * tr + 2

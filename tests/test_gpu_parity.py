@@ -861,3 +861,43 @@ def test_auto_small_calls_take_the_generic_kernel():
                               kernel="pipe")
         assert pinned.launch_info(N)["kernel"] == 3
         pinned.close()
+
+
+@pytest.mark.parametrize("name,N,kernel,fused", [("c2", 32, "auto", False), ("c3", 23, "auto", True),
+                                                 ("c1", 1, "auto", False), ("c2", 32, "dense", False),
+                                                 ("c4_80", 3, "pipe", False)])
+def test_cuda_graph_capture_and_replay(name, N, kernel, fused):
+    """Forward calls captured into a CUDA graph (torch.cuda.graph) and replayed: the
+    stream-K workspace and the padded staging copy become stream-ordered allocations
+    inside the graph; every replay gives the oracle's bits (launch-bound small layers
+    and multi-layer blocks are meant to be replayed this way)."""
+    cfg = synthgen.CONFIGS[name].with_batch(N)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    layer = _layer(cfg, c, b, kernel)
+    x = torch.from_numpy(L.x).cuda()
+    args = (L.x, cfg.F, cfg.K, cfg.stride, cfg.pad, c.rowptr, c.colidx, c.values, b)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up outside the capture
+        out = layer.fused_relu_maxpool(x) if fused else layer(x)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = layer.fused_relu_maxpool(x) if fused else layer(x)
+    for _ in range(3):
+        if fused:
+            out[0].zero_()
+        else:
+            out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        if fused:
+            rp, ra = oracle.fused_f32(*args)
+            assert np.array_equal(bits(out[0].cpu().numpy()), bits(rp)) and np.array_equal(out[1].cpu().numpy(), ra)
+        else:
+            assert np.array_equal(bits(out.cpu().numpy()), bits(oracle.conv_f32(*args)))
+    del g
+    layer.close()
