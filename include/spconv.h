@@ -204,7 +204,9 @@ typedef struct {
     int channels_per_stage; /* pipe: input channels per pipeline stage            */
     int stages;             /* pipe: pipeline depth (shared-memory ring)          */
     int launches;           /* kernel launches per call                           */
-    int reserved[7];
+    int tile_rows;          /* pipe: output rows per thread tile (8, or 7 for conv-only
+                               calls on heights that are multiples of 7)            */
+    int reserved[6];
 } spconv_launch_info_t;
 int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spconv_launch_info_t *info);
 

@@ -34,7 +34,7 @@ import os
 import sys
 
 # (R, T, S) variants instantiated by kernel_pipe.cu
-VARIANTS = [(4, 4, 8), (4, 8, 4), (4, 4, 4), (2, 8, 4)]
+VARIANTS = [(4, 4, 8), (4, 8, 4), (4, 4, 4), (2, 8, 4), (4, 7, 4), (2, 7, 4)]
 MASK_VARIANTS = [(4, 8, 4)]
 # dispatcher code variants (A/B via -DSPC_DISPATCH_VARIANT=v): 0 = round-1 walk,
 # 1 = sp advanced in the case head (no write-after-read stall at the case end),

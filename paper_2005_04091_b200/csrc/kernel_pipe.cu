@@ -548,6 +548,10 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
                     SPC2_DISPATCH_R4T4S8(acc, xw, sp, wp, ch_bytes, row_bytes);
                 } else if constexpr (R == 2 && PT == 8 && PS == 4) {
                     SPC2_DISPATCH_R2T8S4(acc, xw, sp, wp, ch_bytes, row_bytes);
+                } else if constexpr (R == 4 && PT == 7 && PS == 4) {
+                    SPC2_DISPATCH_R4T7S4(acc, xw, sp, wp, ch_bytes, row_bytes);
+                } else if constexpr (R == 2 && PT == 7 && PS == 4) {
+                    SPC2_DISPATCH_R2T7S4(acc, xw, sp, wp, ch_bytes, row_bytes);
                 } else {
                     static_assert(R == 4 && PT == 8 && PS == 4, "no dispatcher generated for this variant");
                     SPC2_DISPATCH_R4T8S4(acc, xw, sp, wp, ch_bytes, row_bytes);
@@ -831,7 +835,7 @@ bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     return K == 3 && stride == 1 && pad == 1 && W + 3 <= 4 * 32;
 }
 
-void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
+void pipe_geometry(const Plan &p, int mode, PipeGeometry &g, int T) {
     // mode 0: TMA on the caller's tensor (xs = 3); 1: TMA on the left-padded copy
     // (xs = 0); 2: cp.async staging (xs = 0)
     g = PipeGeometry{};
@@ -839,8 +843,10 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
     g.xs = mode == 0 ? 3 : 0;
     // 32-pixel thread tiles: 16 FFMA2 per nonzero (scripts/probes/dispatch_probe.cu).
     // 8x4 (tall) keeps the window's 128-bit loads at a 16-byte lane stride (fewer bank
-    // conflicts than 4x8, measured 11.3 vs 9.5 TFLOP/s on c2); only 8x4 is instantiated.
-    g.T = 8;
+    // conflicts than 4x8, measured 11.3 vs 9.5 TFLOP/s on c2).  T = 7 (7x4 tiles) serves
+    // conv-only calls on images whose height is a multiple of 7 but not of 8 (c4's 14x14,
+    // VGG's 28x28): 100% instead of 87.5% row coverage.
+    g.T = T;
     g.S = 4;
     const int PT = g.T, PS = g.S;
     g.tiles_x = (p.Wo + g.xs + PS - 1) / PS;
@@ -873,30 +879,40 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g) {
     g.cc = p.pipe_cc;
     // smem columns read: window of the last tile ends at 4*(tiles_x-1) + 5
     const int need = ((PS * g.tiles_x + 2) + 3) & ~3;
-    int best = need, best_wf = 1 << 30, best_order = 0;
+    int best = need, best_wf = 1 << 30, best_order = 0, best_rs = g.rs;
     // the lane order matters only with several images AND several tile rows per unit
     // (c4: 4 images x 2 tile rows: the pitch alone cannot separate the quarter-warp's
     // two tile rows, 8*pitch = 0 mod 32 words; the image slots can be: 12 -> 8
-    // wavefronts per window row)
+    // wavefronts per window row).  The slots' row count may also be padded by up to 3
+    // rows (staged but unused) when that separates them (c4 with 7-row tiles: 16 rows
+    // per slot put every slot on the same banks, 18 do not); band slots are not padded
+    // (a band's start row is derived from rs).
     const int orders = (g.ipb > 1 && g.tr > 1) ? 2 : 1;
-    for (int order = 0; order < orders; ++order) {
-        g.lane_order = order;
-        for (int cand = need; cand <= need + 32; cand += 4) {
-            // band mode stages every band with its own TMA box into slot b of the stage:
-            // slots must start on 128-byte boundaries (the tensor-copy destination
-            // alignment), i.e. cc * rs * pitch words must be a multiple of 32 (a pitch
-            // multiple of 16 words always qualifies, and the range holds two)
-            if (g.band && (g.cc * g.rs * cand) % 32 != 0) continue;
-            const int wf = window_wavefronts(g, cand);
-            if (wf < best_wf) {
-                best_wf = wf;
-                best = cand;
-                best_order = order;
+    const int rs0 = g.rs, extra_rows = (g.band || g.ipb == 1) ? 0 : 3;
+    for (int extra = 0; extra <= extra_rows; ++extra) {
+        g.rs = rs0 + extra;
+        for (int order = 0; order < orders; ++order) {
+            g.lane_order = order;
+            for (int cand = need; cand <= need + 32; cand += 4) {
+                // band mode stages every band with its own TMA box into slot b of the stage:
+                // slots must start on 128-byte boundaries (the tensor-copy destination
+                // alignment), i.e. cc * rs * pitch words must be a multiple of 32 (a pitch
+                // multiple of 16 words always qualifies, and the range holds two)
+                if (g.band && (g.cc * g.rs * cand) % 32 != 0) continue;
+                const int wf = window_wavefronts(g, cand);
+                // fewest wavefronts; among equals the smallest staged box
+                if (wf < best_wf || (wf == best_wf && g.rs * cand < best_rs * best)) {
+                    best_wf = wf;
+                    best = cand;
+                    best_order = order;
+                    best_rs = g.rs;
+                }
             }
         }
     }
     g.pitch = best;
     g.lane_order = best_order;
+    g.rs = best_rs;
     if (g.band && (g.cc * g.rs * g.pitch) % 32 != 0) return; // (unreachable: see the search)
     if (tma && (g.pitch > 256 || g.rs > 256)) return;
     if (mode == 0 && (p.W * 4) % 16 != 0) return;
@@ -1048,7 +1064,7 @@ cudaError_t stream_k_workspace(const Plan &p, cudaStream_t s, size_t part_bytes,
 // The launch schedule of one forward of N images (staging mode, units, persistent
 // grid, stream-K): the single source of these decisions for launch_pipe and for the
 // spconv_launch_info query the tests assert on.
-bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q) {
+bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only) {
     q = PipeSchedule{};
     // staging: 0 = TMA on the caller's tensor (tile columns shifted by 3),
     //          1 = TMA on a left-padded copy (no shift), 2 = cp.async (fallback)
@@ -1057,7 +1073,13 @@ bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q) {
     if (p.knobs.staging == 2) mode = 2;
     if (p.knobs.staging == 1 && p.pipe_pad.ok) mode = 1;
     if (mode != 2 && get_encode() == nullptr) mode = 2;
-    const PipeGeometry &g = mode == 0 ? p.pipe_tma : mode == 1 ? p.pipe_pad : p.pipe_cp;
+    const PipeGeometry *gp = mode == 0 ? &p.pipe_tma : mode == 1 ? &p.pipe_pad : &p.pipe_cp;
+    // non-fused calls take the 7-row-tile geometry when the plan has one (TMA modes)
+    if (conv_only && p.pipe_dispatch == 0 && mode != 2) {
+        const PipeGeometry &g7 = mode == 0 ? p.pipe7_tma : p.pipe7_pad;
+        if (g7.ok) gp = &g7;
+    }
+    const PipeGeometry &g = *gp;
     if (!g.ok) return false;
     q.mode = mode;
     q.g = &g;
@@ -1079,7 +1101,8 @@ bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q) {
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
                         cudaStream_t s, const float *res, int epi) {
     PipeSchedule sched;
-    if (!pipe_schedule(p, N, reinterpret_cast<uintptr_t>(x), sched)) return cudaErrorInvalidConfiguration;
+    if (!pipe_schedule(p, N, reinterpret_cast<uintptr_t>(x), sched, !fused))
+        return cudaErrorInvalidConfiguration;
     const int mode = sched.mode;
     const PipeGeometry &g = *sched.g;
     const int Wp = ((p.W + 2) + 3) & ~3;
@@ -1177,6 +1200,20 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         else if (epi == 1) { SPC_PIPE_MODES(4, 8, 4, false, 0, 1) }
         else if (epi == 2) { SPC_PIPE_MODES(4, 8, 4, false, 0, 2) }
         else { SPC_PIPE_MODES(4, 8, 4, false, 0, 3) }
+    } else if (g.T == 7 && g.S == 4 && !fused && p.pipe_dispatch == 0 && mode != 2) {
+        // 7x4 tiles: not fused (pool windows would straddle tiles), TMA staging
+        // (pipe_schedule picks them only then); conv and the block epilogues
+#define SPC_PIPE7(RR, EE)                                                                                  \
+    err = mode == 0 ? launch_one<RR, 7, 4, false, 3, 0, 1, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0) \
+                    : launch_one<RR, 7, 4, false, 0, 0, 1, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0);
+        if (p.R == 4) {
+            if (epi == 0) { SPC_PIPE7(4, 0) } else if (epi == 1) { SPC_PIPE7(4, 1) }
+            else if (epi == 2) { SPC_PIPE7(4, 2) } else { SPC_PIPE7(4, 3) }
+        } else {
+            if (epi == 0) { SPC_PIPE7(2, 0) } else if (epi == 1) { SPC_PIPE7(2, 1) }
+            else if (epi == 2) { SPC_PIPE7(2, 2) } else { SPC_PIPE7(2, 3) }
+        }
+#undef SPC_PIPE7
     } else if (p.R == 2 && g.T == 8 && g.S == 4 && p.pipe_dispatch == 0) {
         if (fused) { SPC_PIPE_MODES(2, 8, 4, true, 0, 0) }
         else if (epi == 0) { SPC_PIPE_MODES(2, 8, 4, false, 0, 0) }

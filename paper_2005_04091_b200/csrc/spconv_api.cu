@@ -378,6 +378,14 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                 cc_try == 1)
                 break;
         }
+        // 7-row tiles for conv-only calls when they cover the image height better than
+        // 8-row ones (c4 14x14, VGG 28x28: 100% vs 87.5% of the rows; the tap streams do
+        // not depend on the tile shape, only the staging geometry does)
+        const int t8 = (p->Ho + 7) / 8 * 8, t7 = (p->Ho + 6) / 7 * 7;
+        if (p->pipe_dispatch == 0 && t7 < t8) {
+            spconv::pipe_geometry(*p, 0, p->pipe7_tma, 7);
+            spconv::pipe_geometry(*p, 1, p->pipe7_pad, 7);
+        }
         if ((st = upload(&p->d_group_rows, grows.data(), grows.size(), p->device_bytes))) return st;
         if ((st = upload(&p->d_chunk_start, cstart.data(), cstart.size(), p->device_bytes))) return st;
         if (p->knobs.debug && p->pipe_dispatch == 0 &&
@@ -590,7 +598,7 @@ static bool small_call_prefers_generic(const Plan *p, int N, uintptr_t x) {
     const double fma = double(N) * p->F * p->Ho * p->Wo * (double(p->nnz) / p->F);
     const double t_generic = 7.0 + 1.2e-6 * fma;
     spconv::PipeSchedule q;
-    if (!spconv::pipe_schedule(*p, N, x, q)) return true;
+    if (!spconv::pipe_schedule(*p, N, x, q, false)) return true;
     const double rounds = std::max(1.0, double(q.nunits) / double(spconv::sm_count_of_current_device()));
     const double p_nonempty = 1.0 - std::pow(1.0 - d, 9.0 * p->R);
     const double t_pipe = 5.0 + rounds * p->C * (0.35 * p_nonempty + 0.075 * 9.0 * p->R * d);
@@ -855,7 +863,7 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
             return SPCONV_OK;
         }
         spconv::PipeSchedule q;
-        if (!spconv::pipe_schedule(*p, N, reinterpret_cast<uintptr_t>(x), q)) return SPCONV_ERR_UNSUPPORTED;
+        if (!spconv::pipe_schedule(*p, N, reinterpret_cast<uintptr_t>(x), q, !fused)) return SPCONV_ERR_UNSUPPORTED;
         info->grid = q.grid;
         info->stream_k = q.sk ? 1 : 0;
         info->units = q.nunits;
@@ -864,6 +872,7 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
         info->channels_per_stage = q.g->cc;
         info->stages = q.g->nstage;
         info->launches = q.launches;
+        info->tile_rows = q.g->T;
     }
     return SPCONV_OK;
 }

@@ -121,6 +121,7 @@ struct Plan {
     int32_t *d_chunk_start = nullptr; // [num_gsets * (nchunks + 1)] byte offsets into d_stream2
     uint4 *d_stream2 = nullptr;    // chunks: header (GPC u32 byte offsets) + 16-byte entries
     PipeGeometry pipe_tma{}, pipe_pad{}, pipe_cp{};
+    PipeGeometry pipe7_tma{}, pipe7_pad{}; // 7x4 tiles for non-fused calls (7-row tiles cover the height better)
     PipeKnobs knobs{};
     // dense path (NEXT-1): conv-only calls of a plan whose kernel is SPCONV_KERNEL_DENSE
     // run the dense kernel on the densified filters; fused / epilogue calls use the pipe
@@ -173,7 +174,7 @@ struct PipeSchedule {
     bool sk = false;                    // ordered stream-K split of the units over the CTAs
     int launches = 1;                   // kernel launches per call
 };
-bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q);
+bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only);
 // Stream-K workspace of one launch (kernel_pipe.cu, shared by the dense kernel).
 constexpr size_t kSkHeader = 32768; // counter slots, then u64 flags; partial sums after
 constexpr int kSkSlots = 64;         // [ticket, finished] pairs, one per launch modulo 64
@@ -193,7 +194,8 @@ int sm_count_of_current_device();
 
 // kernel_pipe.cu
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad);
-void pipe_geometry(const Plan &p, int mode, PipeGeometry &g); // mode: 0 TMA, 1 TMA on padded copy, 2 cp.async
+// mode: 0 TMA, 1 TMA on padded copy, 2 cp.async; T: output rows per thread tile (8, or 7)
+void pipe_geometry(const Plan &p, int mode, PipeGeometry &g, int T = 8);
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                         bool fused, cudaStream_t s, const float *res = nullptr, int epi = 0);
 

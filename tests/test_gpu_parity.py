@@ -901,3 +901,38 @@ def test_cuda_graph_capture_and_replay(name, N, kernel, fused):
             assert np.array_equal(bits(out.cpu().numpy()), bits(oracle.conv_f32(*args)))
     del g
     layer.close()
+
+
+@pytest.mark.parametrize("name,N,R", [("c4_80", 3, "4"), ("c4_50", 2, "2"), ("c4_95", 76, "4")])
+def test_pipe_seven_row_tiles(name, N, R, monkeypatch):
+    """Non-fused calls on 14-row images use 7x4 thread tiles (launch info says so; 100% row
+    coverage instead of 87.5%); fused calls on the same plan keep 8x4 tiles.  Bits equal
+    to the oracle for both, R = 4 and R = 2, with stream-K (c4_95 N=76)."""
+    monkeypatch.setenv("SPCONV_PIPE_R", R)
+    cfg = synthgen.CONFIGS[name]
+    L = synthgen.make_layer(cfg.with_batch(N), with_input=False)
+    layer = _layer(cfg.with_batch(N), L.csr, _bias(cfg), "pipe")
+    assert layer.launch_info(N)["tile_rows"] == 7
+    assert layer.launch_info(N, fused=True)["tile_rows"] == 8
+    layer.close()
+    _check_full(cfg, "pipe", False, N=N, f64=False)
+    _check_full(cfg, "pipe", True, N=min(N, 3), f64=False)
+
+
+def test_pipe_seven_row_tiles_vgg_shape():
+    """A VGG-like 28x28 layer (TMA directly on the caller's rows: 7x4 tiles with the -3
+    column shift) and a block epilogue on it (8x4 tiles): bitwise."""
+    cfg = synthgen.LayerConfig(8, "vgg28", 3, 24, 28, 28, 40, 3, 1, 1, 0.2, False, True)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    b = _bias(cfg)
+    layer = _layer(cfg, c, b, "pipe")
+    x = torch.from_numpy(L.x).cuda()
+    assert layer.launch_info(cfg.N, False, x)["tile_rows"] == 7
+    y = layer(x).cpu().numpy()
+    assert np.array_equal(bits(y), bits(oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)))
+    r = torch.from_numpy(synthgen.make_input(tuple(y.shape), 31)).cuda()
+    ye = layer.forward_ex(x, relu=True, residual=r).cpu().numpy()
+    ref = oracle.conv_ex_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, residual=r.cpu().numpy(), relu=True)
+    assert np.array_equal(bits(ye), bits(ref))
+    layer.close()
