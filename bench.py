@@ -229,6 +229,17 @@ def _config(cfg, world, l2note, n_local=None, global_batch=None, scaling="weak")
             "parallelism": f"batch-sharded dp{world} ({scaling} scaling)", "l2": l2note}
 
 
+def rank_images(n_config: int, world: int, rank: int, scaling: str):
+    """[b0, b1) global image indices of this rank and the global batch: weak scaling gives
+    every rank the config's whole batch (images rank*N .. rank*N+N-1 of the counter
+    stream); strong scaling splits the config's batch in contiguous shards."""
+    from paper_2005_04091_b200.parallel import shard_bounds
+    if scaling == "strong":
+        b0, b1 = shard_bounds(n_config, world, rank)
+        return b0, b1, n_config
+    return rank * n_config, (rank + 1) * n_config, n_config * world
+
+
 def _median_max(vals_ms, dev, world):
     """Median of this rank's per-step times, then the max over ranks."""
     import torch
@@ -246,7 +257,7 @@ def run_native(args, cfg):
     import torch.distributed as dist
 
     from paper_2005_04091_b200 import SparseConv2d, spconv
-    from paper_2005_04091_b200.parallel import broadcast_csr, shard_bounds
+    from paper_2005_04091_b200.parallel import broadcast_csr
 
     world, rank, local = _dist_env()
     if not torch.cuda.is_available():
@@ -262,12 +273,7 @@ def run_native(args, cfg):
 
     # ---- this rank's images: weak = the config's full batch per rank, strong = a
     # contiguous shard of the config's batch
-    if args.scaling == "strong":
-        b0, b1 = shard_bounds(cfg.N, world, rank)
-        global_batch = cfg.N
-    else:
-        b0, b1 = rank * cfg.N, (rank + 1) * cfg.N
-        global_batch = cfg.N * world
+    b0, b1, global_batch = rank_images(cfg.N, world, rank, args.scaling)
     n_local = b1 - b0
     lcfg = cfg.with_batch(max(n_local, 1))
 

@@ -401,6 +401,25 @@ bool dense_stream_k(const Plan &p, int64_t nunits, int grid) {
     return nunits > grid && nunits % grid != 0 && nunits < 16 * int64_t(grid);
 }
 
+// Relative efficiency the dense kernel's geometry allows on this layer (1 = every lane
+// tile full and every SM busy): the covered-pixel share of the lane tiles times the
+// share of SMs a single round of units keeps busy (stream-K balances larger counts).
+// AUTO's dense decision uses it (spconv_api.cu): measured dense efficiency 0.68-0.70 of
+// peak on the c2 / c5 shapes (estimate 0.95) vs 0.51 on c4 (estimate 0.76).
+double dense_expected_efficiency(const Plan &p, int N) {
+    DenseGeometry g;
+    dense_geometry(p, g);
+    if (!g.ok) return 0.0;
+    const double covered = g.ipb > 1 ? double(g.LY * g.LR) * DT * g.S                       // one unit
+                                     : double(g.bpi) * g.LY * DT * g.LR * g.S;               // one image
+    const double useful = g.ipb > 1 ? double(g.ipb) * p.Ho * p.Wo : double(p.Ho) * p.Wo;
+    const int64_t blocks = g.ipb > 1 ? (N + g.ipb - 1) / g.ipb : int64_t(N) * g.bpi;
+    const int64_t units = blocks * g.fsets;
+    const int sms = 148;
+    const double waves = units >= sms ? 0.95 : double(units) / sms;
+    return useful / covered * waves;
+}
+
 bool dense_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     (void)C; (void)H; (void)F;
     return K == 3 && stride == 1 && pad == 1 && W <= 224; // 32 lanes x 7 columns
@@ -434,7 +453,8 @@ void dense_geometry(const Plan &p, DenseGeometry &g) {
     // channels per stage: ~40 KB of input box + weights, all stages in ~200 KB
     const int min_pitch = ((g.S * g.LR + 4 + 2) + 3) & ~3;
     const int per_ch = g.ipb * g.rows * (min_pitch + 32) * 4 + DW * 9 * DR * 4;
-    g.cc = std::max(1, std::min(p.C, 40960 / per_ch));
+    const int target = p.knobs.dense_stage > 0 ? p.knobs.dense_stage : 40960;
+    g.cc = std::max(1, std::min(p.C, target / per_ch));
     for (int d = g.cc; d >= 1; --d) // a divisor of C close to cc (no zero-padded tail chunk)
         if (p.C % d == 0) {
             if (2 * d >= g.cc) g.cc = d;

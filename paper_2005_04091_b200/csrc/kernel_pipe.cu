@@ -825,6 +825,7 @@ void read_pipe_knobs(PipeKnobs &k) {
     if (const char *e = std::getenv("SPCONV_PIPE_TRACE")) std::snprintf(k.trace, sizeof(k.trace), "%s", e);
     if (const char *e = std::getenv("SPCONV_PIPE_PROF")) std::snprintf(k.prof, sizeof(k.prof), "%s", e);
     if (const char *e = std::getenv("SPCONV_DEBUG")) k.debug = e[0] == '1';
+    if (const char *e = std::getenv("SPCONV_DENSE_STAGE_BYTES")) k.dense_stage = std::max(4096, std::atoi(e));
 }
 
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {

@@ -530,8 +530,14 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
     p->auto_kernel = o.kernel == SPCONV_KERNEL_AUTO;
     if (o.kernel == SPCONV_KERNEL_AUTO) {
         p->kernel = pipe_ok ? SPCONV_KERNEL_PIPE : tiled_ok ? SPCONV_KERNEL_TILED : SPCONV_KERNEL_GENERIC;
-        // the dense kernel at and above the measured break-even density (DESIGN.md NEXT-1)
-        p->dense = dense_ok && density >= spconv::kDenseBreakEven;
+        // the dense kernel at and above the measured break-even density,
+        // which depends on how well the dense kernel's geometry fits the layer (judged at
+        // a 32-image batch)
+        if (dense_ok && density >= spconv::kDenseBreakEven) {
+            const double eff = spconv::dense_expected_efficiency(*p, 32);
+            p->dense = density >= (eff >= spconv::kDenseGoodGeometry ? spconv::kDenseBreakEven
+                                                                       : spconv::kDenseBreakEvenWeak);
+        }
     } else if (o.kernel == SPCONV_KERNEL_DENSE) {
         // fused / epilogue calls of a dense plan take AUTO's sparse kernel
         p->kernel = pipe_ok ? SPCONV_KERNEL_PIPE : tiled_ok ? SPCONV_KERNEL_TILED : SPCONV_KERNEL_GENERIC;

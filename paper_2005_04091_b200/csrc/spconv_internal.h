@@ -74,6 +74,7 @@ struct PipeKnobs {
     char trace[256] = {}; // SPCONV_PIPE_TRACE=<file>: per-CTA timestamps (debug, synchronises)
     char prof[256] = {};  // SPCONV_PIPE_PROF=<file>: phase clock sums (-DSPC_PROF builds only)
     int debug = 0;        // SPCONV_DEBUG=1: plan self-check at create, synchronise + check every call
+    int dense_stage = 0;  // SPCONV_DENSE_STAGE_BYTES: dense kernel input + weight bytes per stage (A/B)
 };
 void read_pipe_knobs(PipeKnobs &k);
 
@@ -199,11 +200,13 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g, int T = 8);
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax,
                         bool fused, cudaStream_t s, const float *res = nullptr, int epi = 0);
 
-// kernel_dense.cu.  AUTO routes conv-only calls of layers at or above this density to
-// the dense kernel: the measured B200 break-even of the sparse pipe kernel against it is
-// 0.45 (c2 shape), 0.46 (c5), 0.56 (c4) (profiles/r02/breakeven_*.jsonl; DESIGN.md
-// NEXT-1; the paper's own CPU figure is 0.435).
-constexpr double kDenseBreakEven = 0.55;
+// kernel_dense.cu.  AUTO routes every call on a layer at or above the break-even density
+// to the dense kernel.  Measured B200 break-even of the sparse pipe kernel against it:
+// 0.45 (c2 shape), 0.46 (c5), 0.77 (c4, where the dense geometry leaves lanes and SMs
+// idle) -- profiles/r02/breakeven_*.jsonl; the paper's own CPU figure is
+// 0.435.  So: 0.5 when the dense geometry's expected efficiency is high
+// (>= 0.8: full lane tiles, every SM busy), else 0.75.
+constexpr double kDenseBreakEven = 0.50, kDenseBreakEvenWeak = 0.75, kDenseGoodGeometry = 0.80;
 bool dense_supported(int C, int H, int W, int F, int K, int stride, int pad);
 void dense_geometry(const Plan &p, DenseGeometry &g);
 std::vector<float> dense_weights(const Plan &p, const DenseGeometry &g, const std::vector<int32_t> &rowptr,
@@ -211,6 +214,7 @@ std::vector<float> dense_weights(const Plan &p, const DenseGeometry &g, const st
 cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
                          cudaStream_t s, const float *res = nullptr, int epi = 0);
 bool dense_stream_k(const Plan &p, int64_t nunits, int grid);
+double dense_expected_efficiency(const Plan &p, int N);
 
 // kernel_tiled.cu
 bool tiled_supported(int C, int H, int W, int F, int K, int stride, int pad);

@@ -84,7 +84,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.spconv_destroy.argtypes = [vp]
     lib.spconv_output_dims.argtypes = [vp, I, I, ctypes.POINTER(ctypes.c_int64)]
     lib.spconv_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
-    lib.spconv_launch_info.argtypes = [vp, I, I, vp, ctypes.POINTER(LaunchInfo)]
+    if hasattr(lib, "spconv_launch_info") or path == os.path.join(_PKG, "libspconv.so"):
+        # (A/B tooling may load an older build through SPCONV_LIB that predates it)
+        lib.spconv_launch_info.argtypes = [vp, I, I, vp, ctypes.POINTER(LaunchInfo)]
     lib.spconv_status_string.argtypes = [I]
     lib.spconv_status_string.restype = ctypes.c_char_p
     lib.spconv_abi_version.argtypes = []
@@ -92,7 +94,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.spconv_last_cuda_error.restype = ctypes.c_char_p
     lib.spconv_debug_decoded.argtypes = [vp, vp, vp, vp]
     for name in EXPORTS:
-        if name not in ("spconv_status_string", "spconv_last_cuda_error"):
+        if name not in ("spconv_status_string", "spconv_last_cuda_error") and hasattr(lib, name):
             getattr(lib, name).restype = I
     _lib = lib
     return lib

@@ -51,3 +51,15 @@ def test_gpus_flag_without_torchrun_prints_one_line():
 def test_gpus_flag_must_match_world_size():
     r = _run({"RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"}, gpus=4)
     assert r.returncode != 0 and "disagrees" in r.stderr
+
+
+def test_rank_images_weak_and_strong():
+    """bench.py's batch per rank: weak = the config's batch on every rank (disjoint image
+    indices of the counter stream), strong = contiguous shards covering the batch once."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.rank_images(32, 4, 2, "weak") == (64, 96, 128)
+    shards = [bench.rank_images(256, 8, r, "strong") for r in range(8)]
+    assert [s[:2] for s in shards] == [(32 * r, 32 * r + 32) for r in range(8)] and shards[0][2] == 256
+    shards = [bench.rank_images(7, 3, r, "strong")[:2] for r in range(3)]
+    assert shards == [(0, 3), (3, 5), (5, 7)]

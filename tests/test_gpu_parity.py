@@ -816,18 +816,20 @@ def test_dense_kernel_random_shapes():
 
 
 def test_auto_routes_dense_layers_to_the_dense_kernel():
-    """AUTO: calls on layers at or above the measured break-even density (0.55) run the
-    dense kernel -- conv, fused and block epilogues -- (plan and launch info say so),
-    sparser layers the pipe kernel."""
+    """AUTO: calls on layers at or above the measured break-even density run the dense
+    kernel -- conv, fused and block epilogues -- (plan and launch info say so), sparser
+    layers the pipe kernel.  The threshold is 0.5 where the dense geometry is efficient
+    (c2 shape: measured break-even 0.45) and 0.75 where it is not (c4: 0.77)."""
     from paper_2005_04091_b200.spconv import SparseConv2d
-    for d, want in ((1.0, 4), (0.6, 4), (0.5, 3), (0.2, 3)):
-        cfg = synthgen.CONFIGS["c2"].with_density(d)
+    for name, d, want in (("c2", 1.0, 4), ("c2", 0.5, 4), ("c2", 0.45, 3), ("c2", 0.2, 3),
+                          ("c4_50", 0.6, 3), ("c4_50", 0.8, 4)):
+        cfg = synthgen.CONFIGS[name].with_density(d)
         L = synthgen.make_layer(cfg, with_input=False)
         layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, L.csr.rowptr, L.csr.colidx, L.csr.values,
                              device=0)
-        assert layer.info["kernel"] == want, d
-        assert layer.launch_info(32)["kernel"] == want, d
-        assert layer.launch_info(32, fused=True)["kernel"] == want, d
+        assert layer.info["kernel"] == want, (name, d)
+        assert layer.launch_info(cfg.N)["kernel"] == want, (name, d)
+        assert layer.launch_info(cfg.N, fused=True)["kernel"] == want, (name, d)
         layer.close()
 
 
