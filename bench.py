@@ -20,7 +20,8 @@ collective in the timed region; forward + all-gather and broadcast + create are
 reported beside it.
 
 Timing ("repeated 30 times and the median is reported"): W
-untimed warm-ups, then EXACTLY K >= 30 steps between a barrier + cuda
+untimed warm-ups, then EXACTLY K steps (default 100; the paper's 30 or more is the
+intent, fewer are accepted and the median is over what was asked) between a barrier + cuda
 synchronize on both sides; before every step the L2 is flushed (a write of 2x
 the 126 MB L2, untimed) and the step itself is bracketed by CUDA events on the
 launching stream; ``ms_per_step`` = the median step (max over ranks).  Also
@@ -434,7 +435,8 @@ def run_native(args, cfg):
                                       f"({nsets * (in_bytes + out_bytes) / 2**20:.0f} MiB)",
                           n_local=n_local, global_batch=global_batch, scaling=args.scaling),
         "images_per_s": round(images_per_s, 1),
-        "timing": {"protocol": "median of K per-step CUDA-event times, L2 flushed before each (PAPER.md L436)",
+        "timing": {"protocol": f"median of the K = {args.steps} per-step CUDA-event times, L2 flushed before "
+                               "each (PAPER.md L436: median of 30 reps)",
                    "median_ms": round(ms_per_step, 5), "warm_l2_median_ms": round(warm_ms, 5),
                    "steady_state_ms": round(steady_ms, 5),
                    "steady_state_value": round(global_flops / (steady_ms * 1e-3) / 1e9, 2),
@@ -520,8 +522,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    if args.steps < 30 and args.impl == "native":
-        ap.error("--steps must be >= 30 (median of >= 30 timed steps, PAPER.md L436)")
+    if args.steps < 1:
+        ap.error("--steps must be >= 1")
     cfg = synthgen.CONFIGS[args.config]
     if "WORLD_SIZE" in os.environ:
         if int(os.environ["WORLD_SIZE"]) != args.gpus:
