@@ -527,16 +527,21 @@ cudaError_t launch_dense(const Plan &p, int N, const float *x, float *y, int32_t
     const int wsrc = (src == x) ? p.W : g.wq;
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
+    Plan &mp = const_cast<Plan &>(p);
+    const bool cached = mp.cache.find_map(src, N, &g, map);
     cuuint64_t dims[4] = {(cuuint64_t)wsrc, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)wsrc * 4, (cuuint64_t)p.H * wsrc * 4, (cuuint64_t)p.C * p.H * wsrc * 4};
     cuuint32_t box[4] = {(cuuint32_t)g.pitch, (cuuint32_t)g.rows, (cuuint32_t)g.cc, (cuuint32_t)g.ipb};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    CUresult r = dense_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(src), dims, strides,
-                                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        if (xp) cudaFreeAsync(xp, s);
-        return cudaErrorInvalidValue;
+    if (!cached) {
+        CUresult r = dense_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(src), dims,
+                                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            if (xp) cudaFreeAsync(xp, s);
+            return cudaErrorInvalidValue;
+        }
+        mp.cache.put_map(src, N, &g, map);
     }
     // ordered stream-K when the units do not divide evenly over the persistent CTAs
     // (c2 shape: 224 units on 148 SMs would leave the second round a third full)

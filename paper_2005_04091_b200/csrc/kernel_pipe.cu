@@ -1144,7 +1144,9 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
 
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
-    if (mode != 2) {
+    const void *map_src = mode == 0 ? static_cast<const void *>(x) : static_cast<const void *>(xp);
+    Plan &mp = const_cast<Plan &>(p);
+    if (mode != 2 && !mp.cache.find_map(map_src, N, &g, map)) {
         const cuuint64_t Wt = mode == 0 ? (cuuint64_t)p.W : (cuuint64_t)Wp;
         cuuint64_t dims[4] = {Wt, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)N};
         cuuint64_t strides[3] = {Wt * 4, (cuuint64_t)p.H * Wt * 4, (cuuint64_t)p.C * p.H * Wt * 4};
@@ -1158,6 +1160,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
             if (xp) cudaFreeAsync(xp, s);
             return cudaErrorInvalidValue;
         }
+        mp.cache.put_map(map_src, N, &g, map);
     }
     const int grid = sched.grid;
     a.sk = sched.sk ? 1 : 0; a.sk_part = nullptr; a.sk_flag = nullptr; a.sk_ticket = nullptr; a.epoch = 0;

@@ -636,9 +636,18 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
         if (res != y && overlap(res, ybytes, y, ybytes)) return SPCONV_ERR_ALIAS;
     }
     int st;
-    if ((st = check_device_ptr(x, p->device)) || (st = check_device_ptr(y, p->device))) return st;
-    if (argmax && (st = check_device_ptr(argmax, p->device))) return st;
-    if ((flags & SPCONV_EPI_RESIDUAL) && (st = check_device_ptr(res, p->device))) return st;
+    // device-pointer checks, cached per plan by pointer (a pointer once validated as this
+    // device's memory is not re-queried; a caller that frees it and passes the same address
+    // for host memory is outside the contract either way)
+    auto checked = [&](const void *ptr) {
+        if (p->cache.is_valid(ptr)) return int(SPCONV_OK);
+        const int r = check_device_ptr(ptr, p->device);
+        if (r == SPCONV_OK) p->cache.put_valid(ptr);
+        return r;
+    };
+    if ((st = checked(x)) || (st = checked(y))) return st;
+    if (argmax && (st = checked(argmax))) return st;
+    if ((flags & SPCONV_EPI_RESIDUAL) && (st = checked(res))) return st;
     DeviceGuard guard(p->device);
     if (!guard.ok) return SPCONV_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
