@@ -415,7 +415,7 @@ double dense_expected_efficiency(const Plan &p, int N) {
     const double useful = g.ipb > 1 ? double(g.ipb) * p.Ho * p.Wo : double(p.Ho) * p.Wo;
     const int64_t blocks = g.ipb > 1 ? (N + g.ipb - 1) / g.ipb : int64_t(N) * g.bpi;
     const int64_t units = blocks * g.fsets;
-    const int sms = 148;
+    const int sms = sm_count_of_current_device();
     const double waves = units >= sms ? 0.95 : double(units) / sms;
     return useful / covered * waves;
 }
@@ -453,7 +453,10 @@ void dense_geometry(const Plan &p, DenseGeometry &g) {
     // channels per stage: ~40 KB of input box + weights, all stages in ~200 KB
     const int min_pitch = ((g.S * g.LR + 4 + 2) + 3) & ~3;
     const int per_ch = g.ipb * g.rows * (min_pitch + 32) * 4 + DW * 9 * DR * 4;
-    const int target = p.knobs.dense_stage > 0 ? p.knobs.dense_stage : 40960;
+    // ~40 KB stages for <= 64 channels (finer chunks balance the stream-K split of the
+    // few units such layers have: c2 shape 147 vs 150 us at 60 KB), ~60 KB above
+    // (fewer stage turnovers: c5 shape 17.1 vs 18.1 ms) -- profiles/r02/dense_stage_ab.jsonl
+    const int target = p.knobs.dense_stage > 0 ? p.knobs.dense_stage : (p.C <= 64 ? 40960 : 61440);
     g.cc = std::max(1, std::min(p.C, target / per_ch));
     for (int d = g.cc; d >= 1; --d) // a divisor of C close to cc (no zero-padded tail chunk)
         if (p.C % d == 0) {

@@ -42,6 +42,9 @@ struct spconv_lstm_s {
     int2 *d_ent = nullptr;
     int nzc = 0, ent_cap = 0;
     int64_t nnz = 0;
+    // A/B knobs, read once at create: SPCONV_LSTM_KERNEL=rowwarp, SPCONV_LSTM_WPC=8|16
+    bool force_rowwarp = false;
+    int force_wpc = 0;
 };
 
 namespace {
@@ -514,6 +517,8 @@ int spconv_lstm_create(spconv_lstm_t *plan, int L, int D, int H, const int32_t *
     }
     spconv_lstm_s *p = new (std::nothrow) spconv_lstm_s;
     if (!p) return SPCONV_ERR_OOM;
+    if (const char *e = std::getenv("SPCONV_LSTM_KERNEL")) p->force_rowwarp = std::strcmp(e, "rowwarp") == 0;
+    if (const char *e = std::getenv("SPCONV_LSTM_WPC")) p->force_wpc = std::atoi(e);
     p->L = L; p->D = D; p->H = H; p->device = device; p->nnz = nnz; p->nzc = nzc; p->ent_cap = ent_cap + 2;
     auto up = [&](auto **dst, const auto &src) -> int {
         const size_t bytes = sizeof(src[0]) * std::max<size_t>(src.size(), 1);
@@ -588,8 +593,7 @@ int spconv_lstm_forward(spconv_lstm_t plan, int T, int B, const float *x, float 
     a.xT = xT; a.hist = hist; a.cst = cst;
     a.L = L; a.D = D; a.H = H; a.T = T; a.B = B; a.nbc = (B + 63) / 64;
     // B >= 32: the z-staged kernel when rows are 16-byte strided (else one warp per row set)
-    const char *kenv = std::getenv("SPCONV_LSTM_KERNEL"); // A/B tooling and tests
-    const bool rowwarp = kenv && std::strcmp(kenv, "rowwarp") == 0;
+    const bool rowwarp = p->force_rowwarp; // A/B tooling and tests (read at create)
     bool staged = !rowwarp && B >= 32 && B % 4 == 0 && H % 8 == 0 && p->d_off;
     // dynamic shared memory: LSTM_NSTG stages x (z tile + entry buffer + row offsets)
     const size_t zent = size_t(ZC) * ZROW + size_t(p->ent_cap) * 8;
@@ -606,8 +610,7 @@ int spconv_lstm_forward(spconv_lstm_t plan, int T, int B, const float *x, float 
             staged = false; // very dense layers: the one-warp-per-unit kernel
         }
     }
-    const char *wenv = std::getenv("SPCONV_LSTM_WPC"); // A/B tooling: force 8 or 16 warps per CTA
-    const int wpc = wenv ? std::atoi(wenv) : 0;
+    const int wpc = p->force_wpc; // A/B tooling: force 8 or 16 warps per CTA (read at create)
     StagedArgs sa;
     sa.off = p->d_off; sa.ent = p->d_ent; sa.nzc = p->nzc; sa.ent_cap = p->ent_cap;
     auto launch = [&](int w, int l0, int ncell) {

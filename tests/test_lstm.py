@@ -88,10 +88,12 @@ def test_gpu_lstm_staged_kernel(L, D, H, T, B, d, monkeypatch):
     net = SparseLSTM(D, H, layers)
     xt = torch.from_numpy(x).cuda()
     h_staged = net(xt, WAVEFRONT).cpu().numpy()
-    monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")
-    h_row = net(xt, WAVEFRONT).cpu().numpy()
+    monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")  # knobs are read when a plan is created
+    net_row = SparseLSTM(D, H, layers)
+    h_row = net_row(xt, WAVEFRONT).cpu().numpy()
     assert np.array_equal(h_staged.view(np.uint32), h_row.view(np.uint32))
     net.close()
+    net_row.close()
 
 
 @pytest.mark.gpu
@@ -102,12 +104,14 @@ def test_gpu_lstm_staged_cta_sizes(wpc, monkeypatch):
         pytest.skip("no CUDA device")
     from paper_2005_04091_b200.lstm import WAVEFRONT, SparseLSTM
     layers, x = synthgen.make_lstm(2, 70, 64, 0.2, 4, 40)
-    net = SparseLSTM(70, 64, layers)
     xt = torch.from_numpy(x).cuda()
-    monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")
+    monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")  # knobs are read when a plan is created
+    net = SparseLSTM(70, 64, layers)
     ref = net(xt, WAVEFRONT).cpu().numpy()
+    net.close()
     monkeypatch.delenv("SPCONV_LSTM_KERNEL")
     monkeypatch.setenv("SPCONV_LSTM_WPC", wpc)
+    net = SparseLSTM(70, 64, layers)
     h = net(xt, WAVEFRONT).cpu().numpy()
     assert np.array_equal(h.view(np.uint32), ref.view(np.uint32))
     net.close()
@@ -144,8 +148,10 @@ def test_gpu_lstm_random_shapes(monkeypatch):
         net = SparseLSTM(D, H, layers)
         xt = torch.from_numpy(x).cuda()
         h_default = net(xt, WAVEFRONT).cpu().numpy()
-        monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")
-        h_row = net(xt, WAVEFRONT).cpu().numpy()
+        monkeypatch.setenv("SPCONV_LSTM_KERNEL", "rowwarp")  # read when a plan is created
+        net_row = SparseLSTM(D, H, layers)
+        h_row = net_row(xt, WAVEFRONT).cpu().numpy()
+        net_row.close()
         monkeypatch.delenv("SPCONV_LSTM_KERNEL")
         if B >= 32:
             assert np.array_equal(h_default.view(np.uint32), h_row.view(np.uint32)), (i, L, D, H, T, B, d)
