@@ -663,7 +663,11 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     else  // the generic kernel serves every epilogue the specialised kernel lacks
         e = fused ? spconv::launch_generic_fused(*p, N, x, y, argmax, s)
                   : spconv::launch_generic_conv(*p, N, x, y, s, res, epi);
-    if (e == cudaSuccess && p->knobs.debug) e = cudaStreamSynchronize(s); // SPCONV_DEBUG: fault at this call
+    if (e == cudaSuccess && p->knobs.debug) { // SPCONV_DEBUG: report a fault at this call
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        if (cap == cudaStreamCaptureStatusNone) e = cudaStreamSynchronize(s); // (not inside a graph capture)
+    }
     return e == cudaSuccess ? SPCONV_OK : cuda_fail(e);
 }
 
