@@ -90,12 +90,13 @@ __global__ void __launch_bounds__(32 * DW, 1) dense_kernel(const __grid_constant
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     const int nblocks = a.ipb > 1 ? (a.N + a.ipb - 1) / a.ipb : a.N * a.bpi;
     const int nunits = nblocks * a.fsets;
     const int nch = a.nchunks;
-    if (threadIdx.x == 0) { // (one barrier for the mbarrier init and the schedule)
+    if (threadIdx.x == 0) {
         Sched q{0, 0, 0, 0, 0, 0, 0, 0};
         if (a.sk) {
             // ordered stream-K: the CTA with arrival ticket b owns chunk steps

@@ -339,14 +339,9 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     // in registers across the dispatcher's asm would cost it registers (measured: one
     // extra MOV on every case's jump-target path, -4% on c5).
 
-    // Prologue, one barrier: thread 0 initialises the mbarriers and takes the work ticket
-    // (an L2 atomic) while the other threads copy the plan tables (global loads) --
-    // after an L2 flush both are memory round trips, so they overlap.
-    struct Sched {
-        int hA, uh, tc0, tC, ut, nf, uf0, hc, tcs, total;
-    };
-    __shared__ Sched sch;
-    __shared__ int s_bid;
+    for (int i = threadIdx.x; i < ncs; i += blockDim.x) s_cstart[i] = __ldg(a.chunk_start + i);
+    for (int i = threadIdx.x; i < a.num_groups * R; i += blockDim.x) s_rows[i] = __ldg(a.group_rows + i);
+    for (int i = threadIdx.x; i < a.F; i += blockDim.x) s_bias[i] = __ldg(a.bias + i);
     if (threadIdx.x == 0) {
         for (int s = 0; s < ns; ++s) {
             mbar_init(smem_u32(&full_bar[s]), STG == 1 ? 1u : 33u);
@@ -354,6 +349,19 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
             done_cnt[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // Programmatic dependent launch: let the next launch on the stream start its
+    // prologue on SMs this grid frees; griddepcontrol.wait (below, after the schedule)
+    // waits for the previous grid.  Without the launch attribute both are no-ops.
+    // Only plan tables (immutable) and this launch's counter slot are touched before.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    struct Sched {
+        int hA, uh, tc0, tC, ut, nf, uf0, hc, tcs, total;
+    };
+    __shared__ Sched sch;
+    __shared__ int s_bid;
+    if (threadIdx.x == 0) {
         // work index.  Stream-K: an arrival ticket from this launch's counter slot
         // (stream_k_workspace: never shared with the launch this one overlaps, so it
         // can be taken before griddepcontrol.wait): CTA b's tail waits only for the
@@ -377,17 +385,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         }
         q.total = q.hA + q.nf * nch + q.tC;
         sch = q;
-    } else {
-        const int t = int(threadIdx.x) - 1, nt = int(blockDim.x) - 1;
-        for (int i = t; i < ncs; i += nt) s_cstart[i] = __ldg(a.chunk_start + i);
-        for (int i = t; i < a.num_groups * R; i += nt) s_rows[i] = __ldg(a.group_rows + i);
-        for (int i = t; i < a.F; i += nt) s_bias[i] = __ldg(a.bias + i);
     }
-    // Programmatic dependent launch: let the next launch on the stream start its
-    // prologue on SMs this grid frees; griddepcontrol.wait (below) waits for the previous
-    // grid.  Without the launch attribute both are no-ops.  Only plan tables (immutable)
-    // and this launch's counter slot are touched before the wait.
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
     // the previous grid (whose outputs x may be, and whose stream-K workspace this
     // launch reuses) must be complete before x or the parked partials are read
