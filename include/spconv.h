@@ -75,7 +75,8 @@ enum {
 
 /* Kernel selection (spconv_create_ex).  AUTO picks the dense kernel for K = 3,
  * stride 1, pad 1 layers at or above the break-even density, else the pipelined
- * kernel when the shape is supported by it (K = 3, stride 1, pad 1, Wo <= 125),
+ * kernel when the shape is supported by it (K = 3, stride 1, pad 1; rows wider than
+ * 125 outputs in column blocks),
  * else the register-tiled v1 kernel when its staging fits shared memory, else the
  * generic kernel.
  * All are CUDA kernels; all obey the same arithmetic contract. */

@@ -62,6 +62,11 @@ struct PipeArgs {
     const char *stream;
     int N, C, H, W, F, Ho, Wo, Po, Qo;
     int xs, tiles_x, tiles_y, ipb, tr, lanes, blocks_y, rs, pitch, nstage, in_words, in_pad, st_bytes;
+    // wide rows: the row is split into colblocks column blocks of cb_tiles tiles (units of
+    // their own); each block's lanes cover one extra tile (tiles_x = cb_tiles + 1) whose
+    // outputs belong to the next block -- computed, not stored, it feeds the fused
+    // epilogue's pool pairs that straddle the block boundary
+    int colblocks, cb_tiles, tiles_total;
     int cc, nchunks;
     int band; // 1: the ipb slots of a unit are tile-row bands of the flattened (image, tile row) sequence
     uint32_t lane_map[32]; // per lane: slot << 16 | tile row << 8 | tile column (lane_tile on the host)
@@ -205,8 +210,8 @@ __device__ __forceinline__ int find_channel(const uint2 *seg, int nent, int cl, 
 // cp.async: called by a whole warp.
 template <int XS, int STG>
 __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeArgs &a, uint32_t smem0,
-                                           uint32_t fb, int s, int k, int n0, int iy0, int c_beg, int c_end,
-                                           int lane) {
+                                           uint32_t fb, int s, int k, int n0, int iy0, int x0, int c_beg,
+                                           int c_end, int lane) {
     const uint32_t stage_bytes = uint32_t(a.in_pad + a.st_bytes);
     const uint32_t dst_in = smem0 + uint32_t(s) * stage_bytes;
     const uint32_t dst_st = dst_in + uint32_t(a.in_pad);
@@ -224,11 +229,11 @@ __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeAr
             for (int b = 0; b < a.ipb; ++b) {
                 const int v = min(n0 + b, nb - 1); // a ragged last unit reloads the last band (not stored)
                 const int n = v / a.tiles_y, ty = v - n * a.tiles_y;
-                tma_load_4d(tmap, fb, dst_in + uint32_t(b) * slot_bytes, XS == 3 ? -4 : 0, ty * (a.rs - 2) - 1,
-                            k * a.cc, n);
+                tma_load_4d(tmap, fb, dst_in + uint32_t(b) * slot_bytes, x0 + (XS == 3 ? -4 : 0),
+                            ty * (a.rs - 2) - 1, k * a.cc, n);
             }
         } else {
-            tma_load_4d(tmap, fb, dst_in, XS == 3 ? -4 : 0, iy0, k * a.cc, n0);
+            tma_load_4d(tmap, fb, dst_in, x0 + (XS == 3 ? -4 : 0), iy0, k * a.cc, n0);
         }
         bulk_load(dst_st, a.stream + c_beg, st_bytes, fb);
     } else {
@@ -250,7 +255,7 @@ __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeAr
                 n = v / a.tiles_y;
                 iyb = (v - n * a.tiles_y) * (a.rs - 2) - 1;
             }
-            const int c = k * a.cc + cl, iy = iyb + r, ix = col - (XS + 1);
+            const int c = k * a.cc + cl, iy = iyb + r, ix = x0 + col - (XS + 1);
             const bool ok = n < a.N && c < a.C && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
             const float *src = ok ? a.x + (((size_t)n * a.C + c) * a.H + iy) * a.W + ix : a.x;
             cp_async_4(dst_in + uint32_t(e) * 4u, src, ok);
@@ -261,12 +266,18 @@ __device__ __forceinline__ void fill_stage(const CUtensorMap *tmap, const PipeAr
 
 // A unit of work = (image group, block of tile rows, group set): decoded here.
 struct Unit {
-    int gs, n0, ty0;
+    int gs, n0, ty0, cb;
 };
+template <bool CB>
 __device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
     Unit r;
     r.gs = u % a.num_gsets;
     u /= a.num_gsets;
+    r.cb = 0;
+    if constexpr (CB) {
+        r.cb = u % a.colblocks;
+        u /= a.colblocks;
+    }
     if (a.band) { // n0 = first band of the unit
         r.ty0 = 0;
         r.n0 = u * a.ipb;
@@ -279,9 +290,12 @@ __device__ __forceinline__ Unit decode_unit(const PipeArgs &a, int u) {
 
 // EPI (conv-only path): bit 0 = ReLU, bit 1 = add a residual tensor; the order is
 // y = ReLU((acc + bias) + residual), two FP32 adds (reading for NEXT-3).
+// EPI bit 2 (any path): wide rows in column blocks (PipeGeometry::colblocks > 1) --
+// a compile-time switch so the common kernels carry none of its index arithmetic.
 template <int R, int PT, int PS, bool FUSED, int XS, int DISP, int STG, int EPI>
 __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap tmap, const PipeArgs a) {
+    constexpr bool CB = (EPI & 4) != 0;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[MAXSTAGE], empty_bar[MAXSTAGE];
     __shared__ int done_cnt[MAXSTAGE];
@@ -328,7 +342,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     // numbered across units so the ring prefetches the next unit's first channels
     // while this unit finishes (and during its epilogue).
     const int nunits = (a.band ? (a.N * a.tiles_y + a.ipb - 1) / a.ipb : ((a.N + a.ipb - 1) / a.ipb) * a.blocks_y) *
-                       a.num_gsets;
+                       (CB ? a.colblocks : 1) * a.num_gsets;
     const int nch = a.nchunks;
     // this CTA's work items, in processing order: [head of unit uh: channels [0, hc),
     // chunks [0, hA)], nf whole units, [tail of unit ut: channels [tcs, C), chunks
@@ -404,9 +418,10 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
             if (j < nf) { u = full_unit(j); ch = k2 - j * nch; }
             else { u = ut; ch = tc0 + (k2 - nf * nch); }
         }
-        const Unit un = decode_unit(a, u);
+        const Unit un = decode_unit<CB>(a, u);
         const int32_t *cs = s_cstart + un.gs * (a.nchunks + 1);
-        fill_stage<XS, STG>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, ch, un.n0, un.ty0 * PT - 1, cs[ch],
+        fill_stage<XS, STG>(&tmap, a, smem0, smem_u32(&full_bar[s]), s, ch, un.n0, un.ty0 * PT - 1,
+                            CB ? un.cb * a.cb_tiles * PS : 0, cs[ch],
                        cs[ch + 1], lane);
     };
     if (warp == 0) {
@@ -441,7 +456,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
             else { u = ut; c0 = tc0; kind = 2; }
         }
         const int c1 = kind == 1 ? hA : nch;
-        const Unit un = decode_unit(a, u);
+        const Unit un = decode_unit<CB>(a, u);
         const int g = un.gs * a.gpc + warp;
         const bool active = g < a.num_groups; // warp-uniform
 
@@ -612,8 +627,10 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
             n = v / a.tiles_y;
             ty = v - n * a.tiles_y;
         }
-        const bool out_ok = lane_ok && n < a.N && ty < a.tiles_y;
-        const int oy0 = ty * PT, ox0 = tx * PS - XS;
+        // (a column block's extra lane computes the next block's first tile: not stored)
+        const bool own = !CB || tx < a.cb_tiles;
+        const bool out_ok = lane_ok && own && n < a.N && ty < a.tiles_y;
+        const int oy0 = ty * PT, ox0 = ((CB ? un.cb * a.cb_tiles : 0) + tx) * PS - XS;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int f = s_rows[g * R + r];
@@ -830,10 +847,10 @@ void read_pipe_knobs(PipeKnobs &k) {
 
 bool pipe_supported(int C, int H, int W, int F, int K, int stride, int pad) {
     (void)C; (void)F; (void)H;
-    // 32-pixel (8x4) tiles, whole tile rows per block: at most 32 tiles across
-    // (Wo + 3 <= 4 * 32).  Inputs whose rows TMA cannot stage directly (W % 4 != 0
-    // or a misaligned base) go through a left-padded copy (launch_pipe).
-    return K == 3 && stride == 1 && pad == 1 && W + 3 <= 4 * 32;
+    // 32-pixel (8x4) tiles; rows wider than 32 tiles (Wo + 3 > 128) are split into
+    // column blocks (pipe_geometry).  Inputs whose rows TMA cannot stage directly
+    // (W % 4 != 0 or a misaligned base) go through a left-padded copy (launch_pipe).
+    return K == 3 && stride == 1 && pad == 1 && W <= 8192;
 }
 
 void pipe_geometry(const Plan &p, int mode, PipeGeometry &g, int T) {
@@ -852,7 +869,16 @@ void pipe_geometry(const Plan &p, int mode, PipeGeometry &g, int T) {
     const int PT = g.T, PS = g.S;
     g.tiles_x = (p.Wo + g.xs + PS - 1) / PS;
     g.tiles_y = (p.Ho + PT - 1) / PT;
-    if (g.tiles_x > 32) return;
+    g.tiles_total = g.tiles_x;
+    g.colblocks = 1;
+    g.cb_tiles = g.tiles_x;
+    if (g.tiles_x > 32) {
+        // wide rows (Wo > 125): column blocks of cb_tiles tiles, each staged with its own
+        // halo; the lanes of a block cover one extra tile (its pool-pair neighbour)
+        g.colblocks = (g.tiles_x + 30) / 31;
+        g.cb_tiles = (g.tiles_x + g.colblocks - 1) / g.colblocks;
+        g.tiles_x = g.cb_tiles + 1; // lanes per tile row
+    }
     const int per_img = g.tiles_x * g.tiles_y;
     if (per_img <= 16) {
         g.ipb = 32 / per_img;
@@ -1065,7 +1091,7 @@ cudaError_t stream_k_workspace(const Plan &p, cudaStream_t s, size_t part_bytes,
 // The launch schedule of one forward of N images (staging mode, units, persistent
 // grid, stream-K): the single source of these decisions for launch_pipe and for the
 // spconv_launch_info query the tests assert on.
-bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only) {
+bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only, int epi) {
     q = PipeSchedule{};
     // staging: 0 = TMA on the caller's tensor (tile columns shifted by 3),
     //          1 = TMA on a left-padded copy (no shift), 2 = cp.async (fallback)
@@ -1082,11 +1108,14 @@ bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv
     }
     const PipeGeometry &g = *gp;
     if (!g.ok) return false;
+    // wide rows (column blocks) are instantiated for TMA staging with the plain
+    // epilogue and the default dispatcher only (launch_pipe)
+    if (g.colblocks > 1 && (mode == 2 || epi != 0 || p.pipe_dispatch != 0)) return false;
     q.mode = mode;
     q.g = &g;
     const int64_t nblocks = g.band ? (int64_t(N) * g.tiles_y + g.ipb - 1) / g.ipb
                                    : (int64_t)((N + g.ipb - 1) / g.ipb) * g.blocks_y;
-    q.nunits = nblocks * p.num_gsets;
+    q.nunits = nblocks * g.colblocks * p.num_gsets;
     if (q.nunits > 0x7fffffff) return false;
     // persistent: one CTA per SM (the register file holds one 8-warp CTA)
     q.grid = int(std::min<int64_t>(q.nunits, sm_count_of_current_device()));
@@ -1102,7 +1131,7 @@ bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
                         cudaStream_t s, const float *res, int epi) {
     PipeSchedule sched;
-    if (!pipe_schedule(p, N, reinterpret_cast<uintptr_t>(x), sched, !fused))
+    if (!pipe_schedule(p, N, reinterpret_cast<uintptr_t>(x), sched, !fused, epi))
         return cudaErrorInvalidConfiguration;
     const int mode = sched.mode;
     const PipeGeometry &g = *sched.g;
@@ -1129,6 +1158,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.N = N; a.C = p.C; a.H = p.H; a.W = p.W; a.F = p.F; a.Ho = p.Ho; a.Wo = p.Wo;
     a.Po = p.Ho / 2; a.Qo = p.Wo / 2;
     a.xs = g.xs; a.tiles_x = g.tiles_x; a.tiles_y = g.tiles_y; a.ipb = g.ipb; a.tr = g.tr;
+    a.colblocks = g.colblocks; a.cb_tiles = g.cb_tiles; a.tiles_total = g.tiles_total;
     a.lanes = g.lanes; a.blocks_y = g.blocks_y; a.rs = g.rs; a.pitch = g.pitch; a.nstage = g.nstage;
     a.in_words = g.in_words; a.in_pad = g.in_pad; a.st_bytes = g.st_bytes;
     a.cc = g.cc; a.nchunks = g.nchunks; a.band = g.band;
@@ -1193,7 +1223,22 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     err = mode == 0 ? launch_one<RR, TT, SS, FF, 3, DD, 1, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0)              \
         : mode == 1 ? launch_one<RR, TT, SS, FF, 0, DD, 1, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0)              \
                     : launch_one<RR, TT, SS, FF, 0, DD, 0, EE>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0);
-    if (p.R == 4 && g.T == 8 && g.S == 4) {
+    if (g.colblocks > 1) {
+        // wide rows: TMA staging, plain epilogue, default dispatcher -- the only
+        // combinations pipe_schedule accepts for them
+#define SPC_PIPE_CB(RR, TT, FF)                                                                          \
+    err = mode == 0 ? launch_one<RR, TT, 4, FF, 3, 0, 1, 4>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0)  \
+                    : launch_one<RR, TT, 4, FF, 0, 0, 1, 4>(map, a, grid, g.smem_bytes, s, p.knobs.pdl != 0);
+        if (mode == 2 || epi != 0 || p.pipe_dispatch != 0) err = cudaErrorNotSupported;
+        else if (fused && g.T == 8) {
+            if (p.R == 4) { SPC_PIPE_CB(4, 8, true) } else { SPC_PIPE_CB(2, 8, true) }
+        } else if (!fused && g.T == 8) {
+            if (p.R == 4) { SPC_PIPE_CB(4, 8, false) } else { SPC_PIPE_CB(2, 8, false) }
+        } else if (!fused && g.T == 7) {
+            if (p.R == 4) { SPC_PIPE_CB(4, 7, false) } else { SPC_PIPE_CB(2, 7, false) }
+        } else err = cudaErrorNotSupported;
+#undef SPC_PIPE_CB
+    } else if (p.R == 4 && g.T == 8 && g.S == 4) {
         if (fused) {
             if (p.pipe_dispatch == 1) { SPC_PIPE_MODES(4, 8, 4, true, 1, 0) }
             else { SPC_PIPE_MODES(4, 8, 4, true, 0, 0) }

@@ -611,6 +611,14 @@ static bool small_call_prefers_generic(const Plan *p, int N, uintptr_t x) {
     return t_generic < 0.8 * t_pipe;
 }
 
+// Whether the pipelined kernel serves this call at all (its block epilogues need the
+// default dispatcher; wide rows have a subset of instantiations -- pipe_schedule).
+static bool pipe_serves(const Plan *p, int N, uintptr_t x, bool fused, int epi) {
+    if (p->kernel != SPCONV_KERNEL_PIPE || (epi && p->pipe_dispatch == 1)) return false;
+    spconv::PipeSchedule q;
+    return spconv::pipe_schedule(*p, N, x, q, !fused, epi);
+}
+
 static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax, bool fused,
                void *stream, const float *res = nullptr, int flags = 0) {
     if (!plan) return SPCONV_ERR_NULLPTR;
@@ -655,7 +663,7 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
     const int epi = fused ? 0 : flags;
     if (p->dense)
         e = spconv::launch_dense(*p, N, x, y, argmax, fused, s, res, epi);
-    else if (p->kernel == SPCONV_KERNEL_PIPE && !(epi && p->pipe_dispatch == 1) &&
+    else if (pipe_serves(p, N, reinterpret_cast<uintptr_t>(x), fused, epi) &&
              !small_call_prefers_generic(p, N, reinterpret_cast<uintptr_t>(x)))
         e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s, res, epi);
     else if (p->kernel == SPCONV_KERNEL_TILED && epi == 0)
@@ -876,7 +884,8 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
     if (p->kernel == SPCONV_KERNEL_PIPE && N > 0) {
         DeviceGuard guard(p->device);
         if (!guard.ok) return SPCONV_ERR_CUDA;
-        if (small_call_prefers_generic(p, N, reinterpret_cast<uintptr_t>(x))) {
+        if (!pipe_serves(p, N, reinterpret_cast<uintptr_t>(x), fused != 0, 0) ||
+            small_call_prefers_generic(p, N, reinterpret_cast<uintptr_t>(x))) {
             info->kernel = SPCONV_KERNEL_GENERIC;
             info->rows_per_group = 0;
             return SPCONV_OK;

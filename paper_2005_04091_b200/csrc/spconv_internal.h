@@ -54,6 +54,9 @@ struct PipeGeometry {
     int ipb, tr;             // images (band: tile-row bands) per block, tile rows per block (per image)
     int band;                // 1: blocks are ipb one-tile-row bands of the flattened (image, tile row) sequence
     int lane_order = 0;      // lane -> tile: 0 slot-major, 1 tile-row-major (kernel_pipe.cu lane_tile)
+    int colblocks = 1;       // wide rows: column blocks per tile row (units of their own)
+    int cb_tiles = 0;        // tiles per column block (the block's lanes add one overlap tile)
+    int tiles_total = 0;     // tiles per output row
     int lanes;               // active lanes per consumer warp = ipb * tr * tiles_x
     int blocks_y;            // blocks per image (ipb == 1) along the tile rows
     int rs;                  // staged input rows per image = 4 * tr + 2
@@ -219,7 +222,7 @@ struct PipeSchedule {
     bool sk = false;                    // ordered stream-K split of the units over the CTAs
     int launches = 1;                   // kernel launches per call
 };
-bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only);
+bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only, int epi = 0);
 // Stream-K workspace of one launch (kernel_pipe.cu, shared by the dense kernel).
 constexpr size_t kSkHeader = 32768; // counter slots, then u64 flags; partial sums after
 constexpr int kSkSlots = 64;         // [ticket, finished] pairs, one per launch modulo 64

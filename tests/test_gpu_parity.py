@@ -183,6 +183,10 @@ EDGE = [
     (2, 7, 9, 20, 5, 3, 1, 1, 1.0, "pipe"),      # dense
     (1, 4, 6, 8, 4, 3, 1, 1, 0.0, "pipe"),       # nnz = 0 -> bias
     (2, 3, 10, 124, 40, 3, 1, 1, 0.2, "pipe"),   # widest supported row (32 tiles), 2 group sets
+    (2, 3, 10, 125, 40, 3, 1, 1, 0.2, "pipe"),   # 32 tiles + shift: 2 column blocks
+    (1, 5, 9, 224, 12, 3, 1, 1, 0.3, "pipe"),    # VGG-wide row: 2 column blocks
+    (1, 4, 6, 226, 9, 3, 1, 1, 0.3, "pipe"),     # wide and W % 4 != 0 (padded copy)
+    (1, 3, 5, 500, 5, 3, 1, 1, 0.5, "pipe"),     # 5 column blocks
     (1, 2, 3, 4, 1, 3, 1, 1, 0.6, "pipe"),       # F = 1
 ]
 
@@ -225,15 +229,15 @@ def test_unaligned_input_uses_cp_async_path(kernel):
 
 def test_very_wide_rows_fall_back_when_tiled_does_not_fit():
     """W = 3300: the tiled kernel's staging ring would need more than the 227 KB of opt-in
-    shared memory, so AUTO must pick the generic kernel at create (not fail every
-    forward) and an explicit tiled request is rejected as unsupported."""
+    shared memory, so an explicit tiled request is rejected as unsupported at create;
+    AUTO takes the pipe kernel (wide rows in column blocks, round 2) -- bitwise."""
     from paper_2005_04091_b200 import SparseConv2d
     from paper_2005_04091_b200.spconv import SpconvError
     cfg = synthgen.LayerConfig(9, "wide", 1, 2, 3, 3300, 3, 3, 1, 1, 0.5, False, True)
     L = synthgen.make_layer(cfg)
     c, b = L.csr, _bias(cfg)
     layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, device=0)
-    assert layer.info["kernel"] == 1  # generic
+    assert layer.info["kernel"] == 3  # pipe
     y = layer(torch.from_numpy(L.x).cuda()).cpu().numpy()
     ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
     assert np.array_equal(bits(y), bits(ref))
@@ -938,3 +942,29 @@ def test_pipe_seven_row_tiles_vgg_shape():
     ref = oracle.conv_ex_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b, residual=r.cpu().numpy(), relu=True)
     assert np.array_equal(bits(ye), bits(ref))
     layer.close()
+
+
+@pytest.mark.parametrize("staging", ["auto", "cp", "pad"])
+@pytest.mark.parametrize("H,W,N,fused", [(32, 224, 12, False), (28, 224, 6, False), (20, 300, 3, True),
+                                         (16, 130, 5, True)])
+def test_pipe_wide_rows_column_blocks(staging, H, W, N, fused, monkeypatch):
+    """Rows wider than 125 outputs run the pipe kernel in column blocks (each staged with
+    its own halo; the lanes of a block cover one extra tile that only feeds the fused
+    pool pairs straddling the block edge): ordered stream-K across (image rows x column
+    blocks) units, 7-row tiles (H=28), both TMA staging paths; cp.async staging is not
+    instantiated for wide rows, so that request runs the generic kernel -- bitwise."""
+    if staging != "auto":
+        monkeypatch.setenv("SPCONV_PIPE_STAGING", staging)
+    cfg = synthgen.LayerConfig(9, "wide", N, 24, H, W, 64, 3, 1, 1, 0.25, fused, True)
+    _check_full(cfg, "pipe", fused, f64=False)
+    if not fused and staging == "auto" and N == 12:
+        L = synthgen.make_layer(cfg, with_input=False)
+        layer = _layer(cfg, L.csr, _bias(cfg), "pipe")
+        info = layer.launch_info(N)
+        assert info["kernel"] == 3 and info["stream_k"] == 1 and info["units"] > info["grid"], info
+        layer.close()
+    if staging == "cp":
+        L = synthgen.make_layer(cfg, with_input=False)
+        layer = _layer(cfg, L.csr, _bias(cfg), "pipe")
+        assert layer.launch_info(N, fused=fused)["kernel"] == 1
+        layer.close()
