@@ -207,7 +207,10 @@ typedef struct {
     int launches;           /* kernel launches per call                           */
     int tile_rows;          /* pipe: output rows per thread tile (8, or 7 for conv-only
                                calls on heights that are multiples of 7)            */
-    int reserved[6];
+    int sk_split;           /* pipe, stream-K: 1 = per-warp cost-balanced split points
+                               (each warp's range walks the same cost), 0 = uniform
+                               channel split (SPCONV_PIPE_SK_SPLIT=uniform)         */
+    int reserved[5];
 } spconv_launch_info_t;
 int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spconv_launch_info_t *info);
 

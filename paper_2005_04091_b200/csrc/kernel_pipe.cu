@@ -86,6 +86,13 @@ struct PipeArgs {
     unsigned long long *trace; // debug (SPCONV_PIPE_TRACE): per CTA 8 timestamps, or null
     int rev;                   // debug (SPCONV_PIPE_REV=1): CTA b does the work of CTA grid-1-b
     unsigned long long *prof;  // diagnostic builds (-DSPC_PROF): per-phase clock sums, or null
+    // per-warp split points (sk_tab = 1; sk_split on the host): boundary b of the
+    // contiguous ranges lies in unit sk_unit[b], at channel sk_ch[b][w] for warp w --
+    // each warp's range then costs the same (its group's taps and reloads), which the
+    // uniform channel split (sk_tab = 0) does not give
+    int sk_tab;
+    int32_t sk_unit[kSkTabCta + 1];
+    uint16_t sk_ch[(kSkTabCta + 1) * kSkTabGpc];
 };
 
 using namespace dev; // mbarrier / TMA / bulk-copy wrappers (async_copy.cuh)
@@ -305,12 +312,13 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
 #ifdef SPC_PROF
     // diagnostic: clock cycles per phase, summed over warps: [0] other (prologue, loop
     // overhead), [1] waiting for a stage, [2] the tap walk, [3] stage release and refill,
-    // [4] park / epilogue and the next unit's setup
-    __shared__ unsigned long long s_prof[5];
-    if (threadIdx.x < 5) s_prof[threadIdx.x] = 0;
+    // [4] epilogue and the next unit's setup, [5] stream-K park, [6] stream-K resume
+    // (wait + partials), [7] end-of-kernel barrier, [8] prologue (to the first stage wait)
+    __shared__ unsigned long long s_prof[9];
+    if (threadIdx.x < 9) s_prof[threadIdx.x] = 0;
     __syncthreads();
     unsigned prof_t = (unsigned)clock();
-    int prof_ph = 0;
+    int prof_ph = 8;
 #define SPC_PROF_MARK(next)                                                    \
     do {                                                                      \
         const unsigned t_ = (unsigned)clock();                                \
@@ -384,8 +392,26 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         const int t = a.sk ? int(atomicAdd(a.sk_ticket, 1u)) : int(blockIdx.x);
         const int bid = a.rev ? int(gridDim.x) - 1 - t : t;
         s_bid = bid;
+        if (tr) tr[5] = (unsigned long long)bid;
         Sched q{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-        if (a.sk) {
+        if (a.sk && a.sk_tab) {
+            // CTA-level structure from the per-warp table: a tail when any warp starts
+            // inside unit sk_unit[bid], a head when any warp ends inside sk_unit[bid+1];
+            // the stages cover the union of the warps' channel ranges
+            const int C = a.C;
+            const int u0 = a.sk_unit[bid], u1 = a.sk_unit[bid + 1];
+            int mx0 = 0, mn0 = C, mx1 = 0;
+            for (int w = 0; w < a.gpc; ++w) {
+                const int c0 = a.sk_ch[bid * kSkTabGpc + w], c1 = a.sk_ch[(bid + 1) * kSkTabGpc + w];
+                mx0 = max(mx0, c0);
+                mn0 = min(mn0, c0);
+                mx1 = max(mx1, c1);
+            }
+            if (mx0 > 0) { q.tcs = mn0; q.ut = u0; q.tc0 = mn0 / a.cc; q.tC = nch - q.tc0; }
+            if (mx1 > 0) { q.hc = mx1; q.uh = u1; q.hA = (mx1 + a.cc - 1) / a.cc; }
+            q.uf0 = u0 + (mx0 > 0 ? 1 : 0);
+            q.nf = u1 - q.uf0;
+        } else if (a.sk) {
             const int C = a.C;
             const int64_t tot = int64_t(nunits) * C;
             const int64_t s0 = tot * bid / gridDim.x, e0 = tot * (bid + 1) / gridDim.x;
@@ -462,6 +488,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
 
         uint64_t acc[R][PT][SH];
         if (kind == 2 && active) {
+            SPC_PROF_MARK(6);
             // resume: wait for CTA b-1's parked accumulators of this warp (it parked
             // them before any other work, so this wait is normally already satisfied)
             const size_t slot = size_t(bid - 1) * a.gpc + warp;
@@ -484,6 +511,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
             __syncwarp();
             if (tr && threadIdx.x == 0) tr[4] = gtimer();
             if (lane == 0) a.sk_flag[slot] = 0ull; // consumed (graph replays reuse the epoch)
+            SPC_PROF_MARK(4);
         } else {
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -504,8 +532,15 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
                 // channels [cl0, cl1) of this stage: all of them except at a stream-K split
                 const int ncl = min(a.cc, a.C - ch * a.cc);
                 int cl0 = 0, cl1 = ncl;
-                if (kind == 1 && ch == c1 - 1) cl1 = hc - ch * a.cc;
-                if (kind == 2 && ch == c0) cl0 = tcs - ch * a.cc;
+                if (kind == 1) { // head: channels [0, this warp's split)
+                    const int h = a.sk_tab ? int(a.sk_ch[(bid + 1) * kSkTabGpc + warp]) : hc;
+                    cl1 = min(ncl, max(0, h - ch * a.cc));
+                }
+                if (kind == 2) { // tail: channels [this warp's split, C)
+                    const int t = a.sk_tab ? int(a.sk_ch[bid * kSkTabGpc + warp]) : tcs;
+                    cl0 = min(ncl, max(0, t - ch * a.cc));
+                }
+                if (cl0 < cl1) { // (a warp's own split may leave it nothing in this stage)
                 if constexpr (DISP == 1) {
                     mask_walk<R, PT, PS>(acc, stage + win_off, stage + a.in_pad + seg_off, st_base + seg_off, ncl,
                                          cl0, cl1, row_bytes, ch_bytes);
@@ -572,6 +607,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
                     SPC2_DISPATCH_R4T8S4(acc, xw, sp, wp, ch_bytes, row_bytes);
                 }
                 }
+                } // cl0 < cl1
             }
             SPC_PROF_MARK(3);
             // release stage s: the last warp to finish with it refills it with stage kk + ns.
@@ -602,6 +638,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         SPC_PROF_MARK(4);
         if (!active) continue;
         if (kind == 1) {
+            SPC_PROF_MARK(5);
             // park: the partial sums go to slot (b, warp) for CTA b+1
             const size_t slot = size_t(bid) * a.gpc + warp;
             ulonglong2 *dst = a.sk_part + slot * (R * PT * SH / 2) * 32 + lane;
@@ -617,6 +654,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
             if (lane == 0)
                 asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.sk_flag + slot), "l"(a.epoch) : "memory");
             if (tr && threadIdx.x == 0) tr[1] = gtimer();
+            SPC_PROF_MARK(4);
             continue;
         }
 
@@ -729,6 +767,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
         }
     }
     }
+    SPC_PROF_MARK(7);
     if (a.sk) {
         // the last CTA to finish resets the arrival counters for the next launch on
         // this workspace (every CTA has taken its ticket by then)
@@ -745,7 +784,7 @@ __global__ void __launch_bounds__(R == 2 ? 32 * MAX_GPC_R2 : 32 * MAX_GPC, 1)
     SPC_PROF_MARK(0);
 #ifdef SPC_PROF
     __syncthreads();
-    if (a.prof && threadIdx.x < 5) atomicAdd(a.prof + threadIdx.x, s_prof[threadIdx.x]);
+    if (a.prof && threadIdx.x < 9) atomicAdd(a.prof + threadIdx.x, s_prof[threadIdx.x]);
 #endif
     if (tr && threadIdx.x == 0) tr[2] = gtimer();
 }
@@ -838,6 +877,7 @@ void read_pipe_knobs(PipeKnobs &k) {
     }
     if (const char *e = std::getenv("SPCONV_PIPE_SK")) k.sk = e[0] == '1' ? 1 : 0;
     if (const char *e = std::getenv("SPCONV_PIPE_REV")) k.rev = e[0] == '1';
+    if (const char *e = std::getenv("SPCONV_PIPE_SK_SPLIT")) k.sk_split = !(std::strcmp(e, "uniform") == 0 || e[0] == '0');
     if (const char *e = std::getenv("SPCONV_PDL")) k.pdl = !(e[0] == '0');
     if (const char *e = std::getenv("SPCONV_PIPE_TRACE")) std::snprintf(k.trace, sizeof(k.trace), "%s", e);
     if (const char *e = std::getenv("SPCONV_PIPE_PROF")) std::snprintf(k.prof, sizeof(k.prof), "%s", e);
@@ -1128,6 +1168,152 @@ bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv
     return true;
 }
 
+// Per-warp stream-K split points.  The uniform split gives every CTA the same number
+// of (unit, channel) steps, but a warp's time is its own group's walk: its taps and
+// window reloads in those channels, which differ between the warps of a CTA (measured
+// on c2: the average warp waits 5% of the kernel at the end for its CTA's slowest) and
+// between CTAs, plus per-item costs (a unit epilogue, a park, a resume; CTAs with an
+// extra whole unit ended ~3 us later).  Here (1) the CTA boundaries B_b are placed so
+// that every CTA's range costs the same T (greedy + bisection on T) in the average
+// warp's walk cost + item costs, and (2) inside the unit of B_b each warp w splits at
+// the channel where ITS cumulative cost reaches its share of the boundary's cumulative
+// cost -- so every warp of every CTA walks the same cost.  Only split points move: every
+// output is still one ascending fma chain (the ordered head/tail hand-off per warp).
+void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
+    const int C = p.C, gpc = p.gpc, ngs = p.num_gsets;
+    const double kEpi = fused ? kSkEpiFused : kSkEpiConv;
+    // per (gset, lane) prefix costs over the channels, and per gset the lane average
+    std::vector<double> pre(size_t(ngs) * gpc * (C + 1), 0.0), apre(size_t(ngs) * (C + 1), 0.0);
+    std::vector<double> wtot(size_t(gpc), 0.0); // per lane: cost of one unit of every gset
+    double atot = 0.0;
+    for (int gs = 0; gs < ngs; ++gs)
+        for (int w = 0; w < gpc; ++w) {
+            double *P = &pre[(size_t(gs) * gpc + w) * (C + 1)];
+            for (int c = 0; c < C; ++c) P[c + 1] = P[c] + p.sk_cost[(size_t(gs) * gpc + w) * C + c];
+            for (int c = 0; c <= C; ++c) apre[size_t(gs) * (C + 1) + c] += P[c] / gpc;
+            wtot[size_t(w)] += P[C];
+        }
+    for (int gs = 0; gs < ngs; ++gs) atot += apre[size_t(gs) * (C + 1) + C];
+    // cumulative cost at step (u, c): whole units before u (gsets cycle) + the prefix in u
+    std::vector<double> agstot(static_cast<size_t>(ngs), 0.0), agcum(static_cast<size_t>(ngs) + 1, 0.0);
+    for (int gs = 0; gs < ngs; ++gs) {
+        agstot[size_t(gs)] = apre[size_t(gs) * (C + 1) + C];
+        agcum[size_t(gs) + 1] = agcum[size_t(gs)] + agstot[size_t(gs)];
+    }
+    auto Fa = [&](int64_t step) {
+        const int64_t u = step / C;
+        const int c = int(step - u * C), gs = int(u % ngs);
+        return double(u / ngs) * atot + agcum[size_t(gs)] + (c ? apre[size_t(gs) * (C + 1) + c] : 0.0);
+    };
+    auto Fw = [&](int w, int64_t step) {
+        const int64_t u = step / C;
+        const int c = int(step - u * C), gs0 = int(u % ngs);
+        double v = double(u / ngs) * wtot[size_t(w)];
+        for (int gs = 0; gs < gs0; ++gs) v += pre[(size_t(gs) * gpc + w) * (C + 1) + C];
+        return v + pre[(size_t(gs0) * gpc + w) * (C + 1) + c];
+    };
+    const int64_t total = U * C;
+    auto cost = [&](int64_t s0, int64_t e0) {
+        double v = Fa(e0) - Fa(s0);
+        if (s0 % C) v += kSkResume;
+        v += kEpi * double(e0 / C - s0 / C); // units finished in (s0, e0]
+        if (e0 % C) v += kSkPark;
+        return v;
+    };
+    // CTA boundaries: CTA b takes the remaining cost / remaining CTAs (each further
+    // split adds a park and a resume), the boundary nearest to that share
+    std::vector<int64_t> B(size_t(G) + 1, 0);
+    int64_t s0 = 0;
+    for (int b = 0; b < G - 1; ++b) {
+        B[size_t(b)] = s0;
+        if (s0 >= total) continue;
+        const double share = (cost(s0, total) + double(G - b - 1) * (kSkPark + kSkResume)) / double(G - b);
+        const int64_t emin = (s0 % C) ? (s0 / C + 1) * C : s0 + 1; // a tail finishes its unit
+        int64_t lo = std::min(emin, total), hi = total;
+        if (cost(s0, lo) <= share) {
+            while (lo < hi) { // largest e with cost(s0, e) <= share
+                const int64_t mid = lo + (hi - lo + 1) / 2;
+                if (cost(s0, mid) <= share) lo = mid; else hi = mid - 1;
+            }
+            if (lo < total && cost(s0, lo + 1) - share < share - cost(s0, lo)) ++lo; // nearest
+        }
+        s0 = lo;
+    }
+    B[size_t(G) - 1] = s0;
+    B[size_t(G)] = total;
+    t.unit.assign(size_t(G) + 1, 0);
+    t.ch.assign((size_t(G) + 1) * gpc, 0);
+    t.unit[size_t(G)] = int32_t(U);
+    for (int b = 1; b < G; ++b) {
+        const int64_t s0 = B[size_t(b)];
+        int64_t u = s0 / C;
+        uint16_t *row = &t.ch[size_t(b) * gpc];
+        if (s0 % C) {
+            // each lane splits where its own cumulative cost reaches its share
+            const double target = Fa(s0) / Fa(total);
+            int mx = 0, mn = C;
+            const int gsu = int(u % ngs);
+            for (int w = 0; w < gpc; ++w) {
+                if (gsu * gpc + w >= p.num_groups) continue; // no group in this unit: set below
+                const double tw = target * Fw(w, total);
+                int c = 0;
+                while (c < C && Fw(w, u * C + c + 1) <= tw) ++c;
+                if (c < C && Fw(w, u * C + c + 1) - tw < tw - Fw(w, u * C + c)) ++c; // nearest
+                row[w] = uint16_t(c);
+                mx = std::max(mx, c);
+                mn = std::min(mn, c);
+            }
+            for (int w = 0; w < gpc; ++w) // idle lanes: inside the active lanes' range
+                if (gsu * gpc + w >= p.num_groups) row[w] = uint16_t(mx);
+            if (mx == 0) { /* every lane at the unit start: no split */ }
+            else if (mn == C) { // every lane at the unit end: boundary at the next unit
+                ++u;
+                for (int w = 0; w < gpc; ++w) row[w] = 0;
+            }
+        }
+        t.unit[size_t(b)] = int32_t(u);
+    }
+    // ranges must stay ordered and cover at least one unit boundary each (no middle
+    // pieces); otherwise fall back to the uniform split
+    bool ok = true;
+    for (int b = 0; b < G && ok; ++b) {
+        const int u0 = t.unit[size_t(b)], u1 = t.unit[size_t(b) + 1];
+        int mx0 = 0, mx1 = 0;
+        for (int w = 0; w < gpc; ++w) {
+            mx0 = std::max(mx0, int(t.ch[size_t(b) * gpc + w]));
+            mx1 = std::max(mx1, int(t.ch[(size_t(b) + 1) * gpc + w]));
+        }
+        if (u1 < u0 || (mx0 > 0 && u1 <= u0)) ok = false; // (u1 == u0 without a tail: head only)
+    }
+    if (!ok) t.unit.clear();
+}
+
+// The per-warp split table of a stream-K launch, computed once per launch shape (cached
+// in the plan): copied to unit / ch (kernel-parameter layout) when given; false = the
+// uniform split (knob off, grid or warps beyond the parameter table, no valid split).
+bool sk_table(const Plan &p, const PipeSchedule &q, int N, bool fused, int32_t *unit, uint16_t *ch) {
+    if (!q.sk || !p.knobs.sk_split || q.grid > kSkTabCta || p.gpc > kSkTabGpc || p.sk_cost.empty()) return false;
+    Plan &mp = const_cast<Plan &>(p);
+    std::lock_guard<std::mutex> lk(mp.cache.mu);
+    Plan::SkTable *t = nullptr;
+    for (auto &e : mp.sk_tab)
+        if (e.N == N && e.grid == q.grid && e.fused == int(fused) && e.geo == q.g) t = &e;
+    if (!t) {
+        t = &mp.sk_tab[mp.sk_tab_next];
+        mp.sk_tab_next = (mp.sk_tab_next + 1) % 4;
+        *t = Plan::SkTable{};
+        sk_split(p, q.nunits, q.grid, fused, *t);
+        t->N = N; t->grid = q.grid; t->fused = int(fused); t->geo = q.g;
+    }
+    if (t->unit.empty()) return false;
+    if (unit)
+        for (int b = 0; b <= q.grid; ++b) {
+            unit[b] = t->unit[size_t(b)];
+            for (int w = 0; w < p.gpc; ++w) ch[b * kSkTabGpc + w] = t->ch[size_t(b) * p.gpc + w];
+        }
+    return true;
+}
+
 cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t *argmax, bool fused,
                         cudaStream_t s, const float *res, int epi) {
     PipeSchedule sched;
@@ -1170,6 +1356,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.gpc = p.gpc; a.num_groups = p.num_groups; a.num_gsets = p.num_gsets;
     a.tma = mode != 2 ? 1 : 0;
     a.ent = 8;
+    a.sk_tab = 0;
     const int64_t nunits = sched.nunits;
 
     CUtensorMap map;
@@ -1201,8 +1388,8 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     a.prof = nullptr;
 #ifdef SPC_PROF
     const char *prof_out = p.knobs.prof;
-    if (prof_out[0] && cudaMalloc(&a.prof, 5 * sizeof(unsigned long long)) == cudaSuccess)
-        cudaMemsetAsync(a.prof, 0, 5 * sizeof(unsigned long long), s);
+    if (prof_out[0] && cudaMalloc(&a.prof, 9 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemsetAsync(a.prof, 0, 9 * sizeof(unsigned long long), s);
 #endif
     SkWorkspace skws;
     if (a.sk) {
@@ -1217,6 +1404,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
         a.sk_flag = skws.flag;
         a.sk_ticket = skws.ticket;
         a.epoch = next_sk_epoch();
+        a.sk_tab = sk_table(p, sched, N, fused, a.sk_unit, a.sk_ch) ? 1 : 0;
     }
     cudaError_t err = cudaErrorInvalidValue;
 #define SPC_PIPE_MODES(RR, TT, SS, FF, DD, EE)                                                           \
@@ -1272,7 +1460,7 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
     }
 #undef SPC_PIPE_MODES
     if (a.trace) {
-        // debug dump: one line per CTA (start, head parked, end, tail wait begin/end in ns; SM id)
+        // debug dump: one line per CTA (blockIdx, SM id, start, head parked, end, tail wait begin/end in ns, work index)
         std::vector<unsigned long long> h(size_t(grid) * 8);
         cudaStreamSynchronize(s);
         cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -1282,8 +1470,8 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
             for (int b = 0; b < grid; ++b) {
                 const unsigned long long *e = &h[size_t(b) * 8];
                 auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
-                std::fprintf(f, "%d %llu %lld %lld %lld %lld %lld\n", b, e[7], rel(e[0]), rel(e[1]), rel(e[2]),
-                             rel(e[3]), rel(e[4]));
+                std::fprintf(f, "%d %llu %lld %lld %lld %lld %lld %llu\n", b, e[7], rel(e[0]), rel(e[1]), rel(e[2]),
+                             rel(e[3]), rel(e[4]), e[5]);
             }
             std::fprintf(f, "--\n");
             std::fclose(f);
@@ -1293,12 +1481,14 @@ cudaError_t launch_pipe(const Plan &p, int N, const float *x, float *y, int32_t 
 #ifdef SPC_PROF
     if (a.prof) {
         // diagnostic: one line per launch: grid, warps, phase cycle sums (see the kernel)
-        unsigned long long h[5];
+        unsigned long long h[9];
         cudaStreamSynchronize(s);
         cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost);
         if (FILE *f = std::fopen(prof_out, "a")) {
-            std::fprintf(f, "grid %d warps %d other %llu wait %llu walk %llu release %llu epilogue %llu\n", grid,
-                         grid * p.gpc, h[0], h[1], h[2], h[3], h[4]);
+            std::fprintf(f,
+                         "grid %d warps %d other %llu wait %llu walk %llu release %llu epilogue %llu park %llu "
+                         "resume %llu endsync %llu prologue %llu\n",
+                         grid, grid * p.gpc, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8]);
             std::fclose(f);
         }
         cudaFree(a.prof);

@@ -263,6 +263,13 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                 }
             }
         }
+        // walk cost of each (group set, warp, channel) for the stream-K split (sk_split)
+        p->sk_cost.assign(size_t(p->num_gsets) * p->gpc * C, 0.0f);
+        for (int g = 0; g < p->num_groups; ++g)
+            for (int c = 0; c < C; ++c) {
+                const size_t k = byc[size_t(g)][size_t(c)].size();
+                p->sk_cost[size_t(g) * C + c] = float(double(k) + (k ? spconv::kSkReload : 0.0) + spconv::kSkChan);
+            }
         // channels per stage: about 80 KB of staged input per stage (fewer stage
         // boundaries: each costs a barrier wait, a header load and a refill)
         p->pipe_cc = 1;
@@ -901,6 +908,7 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
         info->stages = q.g->nstage;
         info->launches = q.launches;
         info->tile_rows = q.g->T;
+        info->sk_split = spconv::sk_table(*p, q, N, fused != 0, nullptr, nullptr) ? 1 : 0;
     }
     return SPCONV_OK;
 }

@@ -75,6 +75,7 @@ struct PipeKnobs {
     int staging = -1;     // SPCONV_PIPE_STAGING: -1 auto, 1 padded copy, 2 cp.async
     int sk = -1;          // SPCONV_PIPE_SK: -1 auto, 0 off, 1 on (when there are more units than CTAs)
     int rev = 0;          // SPCONV_PIPE_REV=1: reversed work order (debug)
+    int sk_split = 1;     // SPCONV_PIPE_SK_SPLIT: 1 per-warp cost-balanced split points (sk_split), 0 uniform
     int pdl = 1;          // SPCONV_PDL=0: launch without programmatic dependent launch
     char trace[256] = {}; // SPCONV_PIPE_TRACE=<file>: per-CTA timestamps (debug, synchronises)
     char prof[256] = {};  // SPCONV_PIPE_PROF=<file>: phase clock sums (-DSPC_PROF builds only)
@@ -192,6 +193,17 @@ struct Plan {
         unsigned seq = 0; // launches on this workspace: the counter slot of launch k is k % kSkSlots
     };
     std::vector<SkSlot> sk_ws;
+    // per-warp stream-K split tables (kernel_pipe.cu sk_split), cached per launch shape
+    // (under sk_mu): a table depends on the units (N, geometry), the grid and the epilogue
+    std::vector<float> sk_cost; // [gset][warp][C]: walk cost of the warp's group in channel c (tap units)
+    struct SkTable {
+        int N = -1, grid = 0, fused = 0;
+        const void *geo = nullptr;
+        std::vector<int32_t> unit;  // [grid + 1]: unit of boundary b
+        std::vector<uint16_t> ch;   // [(grid + 1) * gpc]: per warp, the split channel in that unit
+    };
+    SkTable sk_tab[4];
+    int sk_tab_next = 0;
     cudaStream_t host_stream = nullptr;    // host -> device copies
     static constexpr int HOST_KSTREAMS = 3;
     cudaStream_t host_kstream[HOST_KSTREAMS] = {}; // forwards of spconv_forward_host (chunks round-robin)
@@ -223,10 +235,23 @@ struct PipeSchedule {
     int launches = 1;                   // kernel launches per call
 };
 bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only, int epi = 0);
+// per-warp stream-K split table of that schedule (kernel_pipe.cu); unit / ch may be null
+bool sk_table(const Plan &p, const PipeSchedule &q, int N, bool fused, int32_t *unit, uint16_t *ch);
 // Stream-K workspace of one launch (kernel_pipe.cu, shared by the dense kernel).
 constexpr size_t kSkHeader = 32768; // counter slots, then u64 flags; partial sums after
 constexpr int kSkSlots = 64;         // [ticket, finished] pairs, one per launch modulo 64
 constexpr size_t kSkFlags = kSkSlots * 8; // byte offset of the flags
+// per-warp split tables travel in the kernel parameters: up to kSkTabCta CTAs and
+// kSkTabGpc warps per CTA (4.5 KB); larger grids use the uniform channel split
+constexpr int kSkTabCta = 160;
+constexpr int kSkTabGpc = 12;
+// walk cost model of the split (units of one tap case, ~125 SM cycles on B200), from
+// per-CTA trace fits (profiles/r02/sk_split_*.txt; c2: a tap case 66 ns, a reload
+// ~4.5 taps, a unit epilogue ~3.0 us conv / ~4.4 us fused): a window reload costs
+// kSkReload taps, a channel of the stage loop kSkChan, and per CTA item a resume,
+// a unit epilogue (conv / fused) or a park
+constexpr double kSkReload = 4.5, kSkChan = 0.6, kSkResume = 20.0, kSkEpiConv = 45.0, kSkEpiFused = 50.0,
+                 kSkPark = 25.0;
 struct SkWorkspace {
     void *base = nullptr;
     bool async = false;                 // a per-call stream-ordered allocation (freed by release)

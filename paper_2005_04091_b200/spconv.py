@@ -58,7 +58,8 @@ class LaunchInfo(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int), ("rows_per_group", ctypes.c_int), ("grid", ctypes.c_int),
                 ("stream_k", ctypes.c_int), ("units", ctypes.c_int64), ("band", ctypes.c_int),
                 ("staging", ctypes.c_int), ("channels_per_stage", ctypes.c_int), ("stages", ctypes.c_int),
-                ("launches", ctypes.c_int), ("tile_rows", ctypes.c_int), ("reserved", ctypes.c_int * 6)]
+                ("launches", ctypes.c_int), ("tile_rows", ctypes.c_int), ("sk_split", ctypes.c_int),
+                ("reserved", ctypes.c_int * 5)]
 
 
 _lib = None

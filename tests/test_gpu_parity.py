@@ -968,3 +968,50 @@ def test_pipe_wide_rows_column_blocks(staging, H, W, N, fused, monkeypatch):
         layer = _layer(cfg, L.csr, _bias(cfg), "pipe")
         assert layer.launch_info(N, fused=fused)["kernel"] == 1
         layer.close()
+
+
+@pytest.mark.parametrize("split", ["auto", "uniform"])
+@pytest.mark.parametrize("case", ["c2", "c3", "ragged", "r2", "skip"])
+def test_pipe_per_warp_stream_k_split(case, split, monkeypatch):
+    """Per-warp stream-K split points (sk_split: every warp of a CTA stops its head and
+    starts its tail at its own channel, so each warp's range walks the same cost): the
+    table is in use (launch info) and the bits equal the oracle's -- the c2 / c3 bench
+    launches; a ragged last group set (F = 40 at R = 4: 8 + 2 warps, idle lanes);
+    R = 2 (11 warps per CTA); rows with nonzeros in every 5th channel only (warps whose
+    split stage holds nothing for them).  SPCONV_PIPE_SK_SPLIT=uniform: the uniform split,
+    same bits."""
+    if split == "uniform":
+        monkeypatch.setenv("SPCONV_PIPE_SK_SPLIT", "uniform")
+    fused = case == "c3"
+    if case in ("c2", "c3"):
+        cfg = synthgen.CONFIGS[case]
+    elif case == "ragged":
+        cfg = synthgen.LayerConfig(9, "ragged", 40, 48, 40, 40, 40, 3, 1, 1, 0.2, False, True)
+    elif case == "r2":
+        monkeypatch.setenv("SPCONV_PIPE_R", "2")
+        cfg = synthgen.CONFIGS["c2"].with_batch(23)
+    else:
+        cfg = synthgen.CONFIGS["c2"].with_batch(23)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    if case == "skip":  # every 5th channel, a different phase per row
+        keep = np.concatenate([((c.colidx[c.rowptr[f]:c.rowptr[f + 1]] // 9) + f) % 5 == 0 for f in range(cfg.F)])
+        counts = [int(np.count_nonzero(keep[c.rowptr[f]:c.rowptr[f + 1]])) for f in range(cfg.F)]
+        c = synthgen.CSR(cfg.F, cfg.C, 3, np.concatenate([[0], np.cumsum(counts)]).astype(np.int32),
+                         c.colidx[keep].astype(np.int32), c.values[keep].astype(np.float32))
+    b = _bias(cfg)
+    layer = _layer(cfg, c, b, "pipe")
+    x = torch.from_numpy(L.x).cuda()
+    info = layer.launch_info(cfg.N, fused, x)
+    assert info["kernel"] == 3 and info["stream_k"] == 1, info
+    assert info["sk_split"] == (1 if split == "auto" else 0), info
+    args = (L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, b)
+    if fused:
+        y, am = layer.fused_relu_maxpool(x)
+        ry, ra = oracle.fused_f32(*args)
+        assert np.array_equal(bits(y.cpu().numpy()), bits(ry))
+        assert np.array_equal(am.cpu().numpy(), ra)
+    else:
+        y = layer(x).cpu().numpy()
+        assert np.array_equal(bits(y), bits(oracle.conv_f32(*args)))
+    layer.close()
