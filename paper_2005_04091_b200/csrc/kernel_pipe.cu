@@ -1186,13 +1186,18 @@ void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
     std::vector<double> pre(size_t(ngs) * gpc * (C + 1), 0.0), apre(size_t(ngs) * (C + 1), 0.0);
     std::vector<double> wtot(size_t(gpc), 0.0); // per lane: cost of one unit of every gset
     double atot = 0.0;
-    for (int gs = 0; gs < ngs; ++gs)
+    for (int gs = 0; gs < ngs; ++gs) {
+        // a unit takes about one warp's walk whatever the number of active warps (the
+        // walk is latency bound): the CTA-level cost averages the ACTIVE lanes only
+        const int act = std::max(1, std::min(gpc, p.num_groups - gs * gpc));
         for (int w = 0; w < gpc; ++w) {
             double *P = &pre[(size_t(gs) * gpc + w) * (C + 1)];
             for (int c = 0; c < C; ++c) P[c + 1] = P[c] + p.sk_cost[(size_t(gs) * gpc + w) * C + c];
-            for (int c = 0; c <= C; ++c) apre[size_t(gs) * (C + 1) + c] += P[c] / gpc;
+            if (w < act)
+                for (int c = 0; c <= C; ++c) apre[size_t(gs) * (C + 1) + c] += P[c] / act;
             wtot[size_t(w)] += P[C];
         }
+    }
     for (int gs = 0; gs < ngs; ++gs) atot += apre[size_t(gs) * (C + 1) + C];
     // cumulative cost at step (u, c): whole units before u (gsets cycle) + the prefix in u
     std::vector<double> agstot(static_cast<size_t>(ngs), 0.0), agcum(static_cast<size_t>(ngs) + 1, 0.0);
