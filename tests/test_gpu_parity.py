@@ -1015,3 +1015,46 @@ def test_pipe_per_warp_stream_k_split(case, split, monkeypatch):
         y = layer(x).cpu().numpy()
         assert np.array_equal(bits(y), bits(oracle.conv_f32(*args)))
     layer.close()
+
+
+def test_random_stream_k_stress_bitwise(monkeypatch):
+    """48 seeded random layers sized so the pipe kernel's units outnumber the SMs (ordered
+    stream-K with per-warp split points), drawn across R = 2 / 4 (ragged group sets),
+    rows wide enough for column blocks, 7- and 8-row tiles, conv and fused, the uniform
+    and the per-warp split: every output (and argmax) bitwise equal to the oracle.  At
+    least a third of the cases must really run stream-K (asserted from the launch info)."""
+    from paper_2005_04091_b200 import SparseConv2d
+    rng = np.random.default_rng(20260418)
+    engaged = 0
+    cases = 48
+    for i in range(cases):
+        R = str(int(rng.choice([2, 4])))
+        split = str(rng.choice(["auto", "uniform"]))
+        monkeypatch.setenv("SPCONV_PIPE_R", R)
+        monkeypatch.setenv("SPCONV_PIPE_SK_SPLIT", split)
+        C = int(rng.integers(4, 20))
+        F = int(rng.integers(9, 70))
+        H = int(rng.choice([14, 21, 24, 28, 30]))
+        W = int(rng.choice([4 * int(rng.integers(4, 30)), 4 * int(rng.integers(32, 66))]))
+        N = int(rng.integers(8, 40))
+        d = float(rng.choice([0.1, 0.2, 0.35]))
+        fused = bool(rng.integers(0, 2))
+        seed = 31000 + 10 * i
+        csr = synthgen.make_csr(F, C, 3, d, seed, seed + 1)
+        xh = synthgen.make_input((N, C, H, W), seed + 2)
+        b = synthgen.make_bias(F, seed + 3)
+        layer = SparseConv2d(C, H, W, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b, kernel="pipe")
+        x = torch.from_numpy(xh).cuda()
+        info = layer.launch_info(N, fused, x)
+        engaged += int(info["kernel"] == 3 and info["stream_k"] == 1)
+        args = (xh, F, 3, 1, 1, csr.rowptr, csr.colidx, csr.values, b)
+        if fused:
+            y, am = layer.fused_relu_maxpool(x)
+            ry, ra = oracle.fused_f32(*args)
+            assert np.array_equal(bits(y.cpu().numpy()), bits(ry)), (i, info)
+            assert np.array_equal(am.cpu().numpy(), ra), (i, info)
+        else:
+            y = layer(x).cpu().numpy()
+            assert np.array_equal(bits(y), bits(oracle.conv_f32(*args))), (i, info)
+        layer.close()
+    assert engaged >= cases // 3, engaged
