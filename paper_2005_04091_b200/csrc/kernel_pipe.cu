@@ -1210,12 +1210,16 @@ void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
         const int c = int(step - u * C), gs = int(u % ngs);
         return double(u / ngs) * atot + agcum[size_t(gs)] + (c ? apre[size_t(gs) * (C + 1) + c] : 0.0);
     };
+    std::vector<double> wcum(size_t(gpc) * (ngs + 1), 0.0); // per lane: units of gsets [0, gs)
+    for (int w = 0; w < gpc; ++w)
+        for (int gs = 0; gs < ngs; ++gs)
+            wcum[size_t(w) * (ngs + 1) + gs + 1] =
+                wcum[size_t(w) * (ngs + 1) + gs] + pre[(size_t(gs) * gpc + w) * (C + 1) + C];
     auto Fw = [&](int w, int64_t step) {
         const int64_t u = step / C;
         const int c = int(step - u * C), gs0 = int(u % ngs);
-        double v = double(u / ngs) * wtot[size_t(w)];
-        for (int gs = 0; gs < gs0; ++gs) v += pre[(size_t(gs) * gpc + w) * (C + 1) + C];
-        return v + pre[(size_t(gs0) * gpc + w) * (C + 1) + c];
+        return double(u / ngs) * wtot[size_t(w)] + wcum[size_t(w) * (ngs + 1) + gs0] +
+               pre[(size_t(gs0) * gpc + w) * (C + 1) + c];
     };
     const int64_t total = U * C;
     auto cost = [&](int64_t s0, int64_t e0) {
@@ -1266,10 +1270,9 @@ void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
             for (int w = 0; w < gpc; ++w) {
                 if (gsu * gpc + w >= p.num_groups) continue; // no group in this unit: set below
                 const double tw = target * Fw(w, total);
-                int c = 0;
-                while (c < C && Fw(w, u * C + c + 1) <= tw) ++c;
-                if (c < C && Fw(w, u * C + c + 1) - tw < tw - Fw(w, u * C + c)) ++c; // nearest
-                c = std::min(chi, std::max(clo, c));
+                int c = clo; // (the result is clamped to [clo, chi] anyway)
+                while (c < chi && Fw(w, u * C + c + 1) <= tw) ++c;
+                if (c < chi && Fw(w, u * C + c + 1) - tw < tw - Fw(w, u * C + c)) ++c; // nearest
                 row[w] = uint16_t(c);
                 mx = std::max(mx, c);
                 mn = std::min(mn, c);
