@@ -278,7 +278,7 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         spconv::pipe_geometry(*p, 1, p->pipe_pad);
         spconv::pipe_geometry(*p, 0, p->pipe_tma);
         const int per_ch = std::max({p->pipe_tma.in_words, p->pipe_pad.in_words, p->pipe_cp.in_words}) * 4;
-        int stage_target = 81920; // measured best on B200
+        int stage_target = 90112; // measured best on B200 (80 KB for c2/c3/c5, 88 KB for c4)
         if (const char *e = std::getenv("SPCONV_PIPE_STAGE_BYTES")) stage_target = std::max(4096, std::atoi(e));
         const bool tma_feasible = p->pipe_tma.ok, pad_feasible = p->pipe_pad.ok;
         std::vector<int32_t> cstart;
