@@ -270,7 +270,7 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
                 const size_t k = byc[size_t(g)][size_t(c)].size();
                 p->sk_cost[size_t(g) * C + c] = float(double(k) + (k ? spconv::kSkReload : 0.0) + spconv::kSkChan);
             }
-        // channels per stage: about 80 KB of staged input per stage (fewer stage
+        // channels per stage: about 88 KB of staged input per stage (fewer stage
         // boundaries: each costs a barrier wait, a header load and a refill)
         p->pipe_cc = 1;
         p->max_chunk_bytes = 0;
@@ -278,7 +278,7 @@ int build_plan(Plan *p, const std::vector<int32_t> &rowptr, const std::vector<in
         spconv::pipe_geometry(*p, 1, p->pipe_pad);
         spconv::pipe_geometry(*p, 0, p->pipe_tma);
         const int per_ch = std::max({p->pipe_tma.in_words, p->pipe_pad.in_words, p->pipe_cp.in_words}) * 4;
-        int stage_target = 90112; // measured best on B200 (80 KB for c2/c3/c5, 88 KB for c4)
+        int stage_target = 90112; // measured on B200: c4 -1.5% vs 80 KB, c2/c3/c5 equal
         if (const char *e = std::getenv("SPCONV_PIPE_STAGE_BYTES")) stage_target = std::max(4096, std::atoi(e));
         const bool tma_feasible = p->pipe_tma.ok, pad_feasible = p->pipe_pad.ok;
         std::vector<int32_t> cstart;
