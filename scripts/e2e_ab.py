@@ -25,10 +25,12 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
                       "config": cfg.name, "ms": round(ms, 4), "tflops": round(cfg.useful_flops / ms / 1e9, 3),
                       "in_MB": px.nbytes / 1e6}), flush=True)
     sys.exit(0)
-libs = sys.argv[1].split(",") if len(sys.argv) > 1 else [""]
-for cfg in ("c2", "c4_80"):
+libs = sys.argv[1].split(",") if len(sys.argv) > 1 and sys.argv[1] else [""]
+configs = os.environ.get("E2E_CONFIGS", "c2,c4_80").split(",")
+chunk_counts = os.environ.get("E2E_CHUNKS", ",1,4,8,16").split(",")
+for cfg in configs:
     for lib in libs:
-        for ch in ("", "1", "4", "8", "16"):
+        for ch in chunk_counts:
             env = dict(os.environ)
             if lib:
                 env["SPCONV_LIB"] = os.path.abspath(lib)

@@ -1,28 +1,52 @@
-"""Probe: pinned H2D / D2H bandwidth alone and concurrently (PCIe duplex) on the box."""
-import torch, time
-n = 25690112 // 4
+"""PCIe copy bandwidth on this box: H2D alone, D2H alone, both at once (pinned host
+buffers, separate streams), for the c2 e2e byte counts (25.7 MB each way): the bound
+of spconv_forward_host's end-to-end number."""
+import json
+import torch
+
+n = 32 * 64 * 56 * 56  # c2 input / output floats
 h_in = torch.empty(n, dtype=torch.float32).pin_memory()
 h_out = torch.empty(n, dtype=torch.float32).pin_memory()
-d_in = torch.empty(n, device="cuda"); d_out = torch.empty(n, device="cuda")
+d_in = torch.empty(n, dtype=torch.float32, device="cuda")
+d_out = torch.empty(n, dtype=torch.float32, device="cuda")
 s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-def t(fn, reps=20):
-    fn(); torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(reps): fn()
+bytes_ = n * 4
+
+
+def timed(fn, reps=20):
+    for _ in range(3):
+        fn()
     torch.cuda.synchronize()
-    return (time.perf_counter() - t0) / reps
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
 def h2d():
-    with torch.cuda.stream(s1): d_in.copy_(h_in, non_blocking=True)
+    d_in.copy_(h_in, non_blocking=True)
+
+
 def d2h():
-    with torch.cuda.stream(s2): h_out.copy_(d_out, non_blocking=True)
-def both(): h2d(); d2h()
-def chunks(k):
-    def f():
-        m = n // k
-        for i in range(k):
-            with torch.cuda.stream(s1): d_in[i*m:(i+1)*m].copy_(h_in[i*m:(i+1)*m], non_blocking=True)
-            with torch.cuda.stream(s2): h_out[i*m:(i+1)*m].copy_(d_out[i*m:(i+1)*m], non_blocking=True)
-    return f
-for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both), ("both_chunk8", chunks(8))):
-    dt = t(fn)
-    print(f"{name}: {dt*1e3:.3f} ms  ({n*4/dt/1e9:.1f} GB/s per direction)")
+    h_out.copy_(d_out, non_blocking=True)
+
+
+def both():
+    cur = torch.cuda.current_stream()
+    s1.wait_stream(cur)
+    s2.wait_stream(cur)
+    with torch.cuda.stream(s1):
+        d_in.copy_(h_in, non_blocking=True)
+    with torch.cuda.stream(s2):
+        h_out.copy_(d_out, non_blocking=True)
+    cur.wait_stream(s1)
+    cur.wait_stream(s2)
+
+
+for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both)):
+    ms = timed(fn)
+    gbps = (2 if name == "both" else 1) * bytes_ / ms / 1e6
+    print(json.dumps({"copy": name, "ms": round(ms, 4), "GB_s_total": round(gbps, 1), "bytes_each_way": bytes_}))
