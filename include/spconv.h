@@ -227,6 +227,17 @@ const char *spconv_last_cuda_error(void);
  * c[j], dy[j] = ky_j - pad, dx[j] = kx_j - pad. */
 int spconv_debug_decoded(spconv_plan_t plan, int32_t *c, int32_t *dy, int32_t *dx);
 
+/* Test-only, host code (no GPU): the per-warp stream-K split points the pipe kernel's
+ * launch would use (DESIGN.md §6 "Per-warp split points") for units work units of C
+ * channel steps on grid CTAs of gpc warps, from cost[(gset*gpc + warp)*C + c] = the
+ * walk cost of that warp's row group in channel c (ngs group sets, num_groups groups;
+ * cc channels per pipeline stage; fused selects the epilogue cost).  Outputs unit[grid+1]
+ * (the unit of boundary b) and ch[(grid+1)*gpc] (warp w's split channel in it).
+ * SPCONV_ERR_SHAPE on bad sizes (grid <= 160, gpc <= 12); SPCONV_ERR_UNSUPPORTED when no
+ * valid split exists (the launch then uses the uniform channel split). */
+int spconv_debug_sk_split(const float *cost, int C, int gpc, int ngs, int num_groups, int cc, int64_t units,
+                          int grid, int fused, int32_t *unit, uint16_t *ch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1179,8 +1179,8 @@ bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv
 // the channel where ITS cumulative cost reaches its share of the boundary's cumulative
 // cost -- so every warp of every CTA walks the same cost.  Only split points move: every
 // output is still one ascending fma chain (the ordered head/tail hand-off per warp).
-void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
-    const int C = p.C, gpc = p.gpc, ngs = p.num_gsets;
+void sk_split_core(const float *lane_cost, int C, int gpc, int ngs, int num_groups, int cc, int64_t U, int G, bool fused,
+                   std::vector<int32_t> &unit_out, std::vector<uint16_t> &ch_out) {
     const double kEpi = fused ? kSkEpiFused : kSkEpiConv;
     // per (gset, lane) prefix costs over the channels, and per gset the lane average
     std::vector<double> pre(size_t(ngs) * gpc * (C + 1), 0.0), apre(size_t(ngs) * (C + 1), 0.0);
@@ -1189,10 +1189,10 @@ void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
     for (int gs = 0; gs < ngs; ++gs) {
         // a unit takes about one warp's walk whatever the number of active warps (the
         // walk is latency bound): the CTA-level cost averages the ACTIVE lanes only
-        const int act = std::max(1, std::min(gpc, p.num_groups - gs * gpc));
+        const int act = std::max(1, std::min(gpc, num_groups - gs * gpc));
         for (int w = 0; w < gpc; ++w) {
             double *P = &pre[(size_t(gs) * gpc + w) * (C + 1)];
-            for (int c = 0; c < C; ++c) P[c + 1] = P[c] + p.sk_cost[(size_t(gs) * gpc + w) * C + c];
+            for (int c = 0; c < C; ++c) P[c + 1] = P[c] + lane_cost[(size_t(gs) * gpc + w) * C + c];
             if (w < act)
                 for (int c = 0; c <= C; ++c) apre[size_t(gs) * (C + 1) + c] += P[c] / act;
             wtot[size_t(w)] += P[C];
@@ -1250,13 +1250,13 @@ void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
     }
     B[size_t(G) - 1] = s0;
     B[size_t(G)] = total;
-    t.unit.assign(size_t(G) + 1, 0);
-    t.ch.assign((size_t(G) + 1) * gpc, 0);
-    t.unit[size_t(G)] = int32_t(U);
+    unit_out.assign(size_t(G) + 1, 0);
+    ch_out.assign((size_t(G) + 1) * gpc, 0);
+    unit_out[size_t(G)] = int32_t(U);
     for (int b = 1; b < G; ++b) {
         const int64_t s0 = B[size_t(b)];
         int64_t u = s0 / C;
-        uint16_t *row = &t.ch[size_t(b) * gpc];
+        uint16_t *row = &ch_out[size_t(b) * gpc];
         if (s0 % C) {
             // each lane splits where its own cumulative cost reaches its share, at most
             // one stage from the CTA-level split: the head and tail stage ranges are
@@ -1264,11 +1264,11 @@ void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
             // the average (R = 2 on c4: 11 group sets, a ragged one) would otherwise
             // stretch both over the whole unit (measured: c4_50 291 -> 406 us)
             const double target = Fa(s0) / Fa(total);
-            const int h = int(s0 % C), clo = std::max(0, h - p.pipe_cc), chi = std::min(C, h + p.pipe_cc);
+            const int h = int(s0 % C), clo = std::max(0, h - cc), chi = std::min(C, h + cc);
             int mx = 0, mn = C;
             const int gsu = int(u % ngs);
             for (int w = 0; w < gpc; ++w) {
-                if (gsu * gpc + w >= p.num_groups) continue; // no group in this unit: set below
+                if (gsu * gpc + w >= num_groups) continue; // no group in this unit: set below
                 const double tw = target * Fw(w, total);
                 int c = clo; // (the result is clamped to [clo, chi] anyway)
                 while (c < chi && Fw(w, u * C + c + 1) <= tw) ++c;
@@ -1278,28 +1278,32 @@ void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
                 mn = std::min(mn, c);
             }
             for (int w = 0; w < gpc; ++w) // idle lanes: inside the active lanes' range
-                if (gsu * gpc + w >= p.num_groups) row[w] = uint16_t(mx);
+                if (gsu * gpc + w >= num_groups) row[w] = uint16_t(mx);
             if (mx == 0) { /* every lane at the unit start: no split */ }
             else if (mn == C) { // every lane at the unit end: boundary at the next unit
                 ++u;
                 for (int w = 0; w < gpc; ++w) row[w] = 0;
             }
         }
-        t.unit[size_t(b)] = int32_t(u);
+        unit_out[size_t(b)] = int32_t(u);
     }
     // ranges must stay ordered and cover at least one unit boundary each (no middle
     // pieces); otherwise fall back to the uniform split
     bool ok = true;
     for (int b = 0; b < G && ok; ++b) {
-        const int u0 = t.unit[size_t(b)], u1 = t.unit[size_t(b) + 1];
+        const int u0 = unit_out[size_t(b)], u1 = unit_out[size_t(b) + 1];
         int mx0 = 0, mx1 = 0;
         for (int w = 0; w < gpc; ++w) {
-            mx0 = std::max(mx0, int(t.ch[size_t(b) * gpc + w]));
-            mx1 = std::max(mx1, int(t.ch[(size_t(b) + 1) * gpc + w]));
+            mx0 = std::max(mx0, int(ch_out[size_t(b) * gpc + w]));
+            mx1 = std::max(mx1, int(ch_out[(size_t(b) + 1) * gpc + w]));
         }
         if (u1 < u0 || (mx0 > 0 && u1 <= u0)) ok = false; // (u1 == u0 without a tail: head only)
     }
-    if (!ok) t.unit.clear();
+    if (!ok) unit_out.clear();
+}
+
+void sk_split(const Plan &p, int64_t U, int G, bool fused, Plan::SkTable &t) {
+    sk_split_core(p.sk_cost.data(), p.C, p.gpc, p.num_gsets, p.num_groups, p.pipe_cc, U, G, fused, t.unit, t.ch);
 }
 
 // The per-warp split table of a stream-K launch, computed once per launch shape (cached

@@ -932,6 +932,21 @@ int spconv_plan_info(spconv_plan_t plan, spconv_plan_info_t *info) {
     return SPCONV_OK;
 }
 
+int spconv_debug_sk_split(const float *cost, int C, int gpc, int ngs, int num_groups, int cc, int64_t units,
+                          int grid, int fused, int32_t *unit, uint16_t *ch) {
+    if (!cost || !unit || !ch) return SPCONV_ERR_NULLPTR;
+    if (C < 1 || gpc < 1 || gpc > spconv::kSkTabGpc || ngs < 1 || num_groups < 1 || num_groups > gpc * ngs ||
+        cc < 1 || units < 1 || grid < 1 || grid > spconv::kSkTabCta)
+        return SPCONV_ERR_SHAPE;
+    std::vector<int32_t> u;
+    std::vector<uint16_t> c;
+    spconv::sk_split_core(cost, C, gpc, ngs, num_groups, cc, units, grid, fused != 0, u, c);
+    if (u.empty()) return SPCONV_ERR_UNSUPPORTED; // no valid split: the launch uses the uniform one
+    std::memcpy(unit, u.data(), u.size() * sizeof(int32_t));
+    std::memcpy(ch, c.data(), c.size() * sizeof(uint16_t));
+    return SPCONV_OK;
+}
+
 int spconv_debug_decoded(spconv_plan_t plan, int32_t *c, int32_t *dy, int32_t *dx) {
     if (!plan) return SPCONV_ERR_NULLPTR;
     const Plan *p = plan;

@@ -237,6 +237,9 @@ struct PipeSchedule {
 bool pipe_schedule(const Plan &p, int N, uintptr_t x, PipeSchedule &q, bool conv_only, int epi = 0);
 // per-warp stream-K split table of that schedule (kernel_pipe.cu); unit / ch may be null
 bool sk_table(const Plan &p, const PipeSchedule &q, int N, bool fused, int32_t *unit, uint16_t *ch);
+// the split itself, from per-(gset, warp, channel) costs (plan-free: spconv_debug_sk_split)
+void sk_split_core(const float *lane_cost, int C, int gpc, int ngs, int num_groups, int cc, int64_t U, int G, bool fused,
+                   std::vector<int32_t> &unit_out, std::vector<uint16_t> &ch_out);
 // Stream-K workspace of one launch (kernel_pipe.cu, shared by the dense kernel).
 constexpr size_t kSkHeader = 32768; // counter slots, then u64 flags; partial sums after
 constexpr int kSkSlots = 64;         // [ticket, finished] pairs, one per launch modulo 64

@@ -28,7 +28,7 @@ EXPORTS = ("spconv_create", "spconv_create_ex", "spconv_forward", "spconv_fused_
            "spconv_forward_host", "spconv_destroy", "spconv_output_dims", "spconv_plan_info",
            "spconv_status_string", "spconv_abi_version", "spconv_debug_decoded",
            "spconv_last_cuda_error", "spconv_forward_ex", "spconv_resize_bilinear",
-           "spconv_resize_fused_relu_maxpool", "spconv_launch_info")
+           "spconv_resize_fused_relu_maxpool", "spconv_launch_info", "spconv_debug_sk_split")
 
 
 class SpconvError(RuntimeError):
@@ -94,6 +94,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.spconv_last_cuda_error.argtypes = []
     lib.spconv_last_cuda_error.restype = ctypes.c_char_p
     lib.spconv_debug_decoded.argtypes = [vp, vp, vp, vp]
+    if hasattr(lib, "spconv_debug_sk_split"):
+        lib.spconv_debug_sk_split.argtypes = [vp, I, I, I, I, I, L, I, I, vp, vp]
     for name in EXPORTS:
         if name not in ("spconv_status_string", "spconv_last_cuda_error") and hasattr(lib, name):
             getattr(lib, name).restype = I
@@ -216,6 +218,18 @@ def spconv_launch_info(plan, N, fused=False, x_ptr=None) -> dict:
     _check(load_library().spconv_launch_info(plan, N, int(bool(fused)), x_ptr, ctypes.byref(info)),
            "spconv_launch_info")
     return {f: getattr(info, f) for f, _ in LaunchInfo._fields_ if f != "reserved"}
+
+
+def spconv_debug_sk_split(cost, C, gpc, ngs, num_groups, cc, units, grid, fused=False):
+    """Test-only host call: the per-warp stream-K split table (unit[grid+1], ch[grid+1, gpc])
+    for a float32 cost array [ngs, gpc, C]; raises SpconvError if no valid split exists."""
+    cost = np.ascontiguousarray(cost, dtype=np.float32)
+    assert cost.shape == (ngs, gpc, C)
+    unit = np.zeros(grid + 1, np.int32)
+    ch = np.zeros((grid + 1, gpc), np.uint16)
+    _check(load_library().spconv_debug_sk_split(_ptr(cost), C, gpc, ngs, num_groups, cc, units, grid,
+                                                int(bool(fused)), _ptr(unit), _ptr(ch)), "spconv_debug_sk_split")
+    return unit, ch
 
 
 def spconv_debug_decoded(plan, nnz):
