@@ -1058,3 +1058,33 @@ def test_random_stream_k_stress_bitwise(monkeypatch):
             assert np.array_equal(bits(y), bits(oracle.conv_f32(*args))), (i, info)
         layer.close()
     assert engaged >= cases // 3, engaged
+
+
+def test_split_tables_for_many_batch_sizes_interleaved():
+    """One plan, six batch sizes (more than the plan's four cached split tables, so
+    entries are recomputed and evicted) launched round-robin on two streams, twice:
+    every output equals the oracle bitwise and each launch used its own table."""
+    from paper_2005_04091_b200 import SparseConv2d, spconv
+    cfg = synthgen.CONFIGS["c2"]
+    Ns = [23, 26, 29, 32, 35, 38]
+    L = synthgen.make_layer(cfg.with_batch(max(Ns)))
+    c = L.csr
+    layer = SparseConv2d(cfg.C, cfg.H, cfg.W, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, None)
+    x = torch.from_numpy(L.x).cuda()
+    ref = oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, None)
+    for N in Ns:
+        info = layer.launch_info(N, False, x)
+        assert info["stream_k"] == 1 and info["sk_split"] == 1, (N, info)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for rep in range(2):
+        for i, N in enumerate(Ns):
+            s = streams[(i + rep) % 2]
+            with torch.cuda.stream(s):
+                y = torch.empty((N, cfg.F, cfg.H, cfg.W), device="cuda")
+                spconv.spconv_forward(layer.plan, N, x.data_ptr(), y.data_ptr(), s)
+                outs.append((N, y))
+    torch.cuda.synchronize()
+    for N, y in outs:
+        assert np.array_equal(bits(y.cpu().numpy()), bits(ref[:N])), N
+    layer.close()
