@@ -74,6 +74,7 @@ int upload(T **dptr, const T *src, size_t n, int64_t &bytes) {
 
 void free_plan(Plan *p) {
     if (!p) return;
+    free_plan(p->alt);
     DeviceGuard g(p->device);
     cudaFree(p->d_rowptr);
     cudaFree(p->d_taps);
@@ -534,6 +535,7 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
         return SPCONV_ERR_UNSUPPORTED;
     }
     const double density = double(nnz) / (double(F) * ncol);
+    p->density = density;
     p->auto_kernel = o.kernel == SPCONV_KERNEL_AUTO;
     if (o.kernel == SPCONV_KERNEL_AUTO) {
         p->kernel = pipe_ok ? SPCONV_KERNEL_PIPE : tiled_ok ? SPCONV_KERNEL_TILED : SPCONV_KERNEL_GENERIC;
@@ -584,6 +586,25 @@ int spconv_create_ex(spconv_plan_t *plan, int C, int H, int W, int F, int K, int
         free_plan(p);
         return st;
     }
+    // the R = 2 alternate of an AUTO pipe plan (prefer_alt chooses per call)
+    if (p->auto_kernel && p->kernel == SPCONV_KERNEL_PIPE && !p->dense && p->R == 4 &&
+        density >= spconv::kAltMinDensity && !std::getenv("SPCONV_PIPE_R") && !std::getenv("SPCONV_NO_ALT")) {
+        spconv_plan_s *q = new (std::nothrow) spconv_plan_s;
+        if (q) {
+            q->C = p->C; q->H = p->H; q->W = p->W; q->F = p->F; q->K = p->K; q->stride = p->stride;
+            q->pad = p->pad; q->Ho = p->Ho; q->Wo = p->Wo; q->nnz = p->nnz; q->device = p->device;
+            q->knobs = p->knobs;
+            q->kernel = SPCONV_KERNEL_PIPE;
+            q->density = density;
+            if (build_plan(q, h_rowptr, h_colidx, h_values, h_bias, 2) == SPCONV_OK) {
+                p->alt = q;
+                p->device_bytes += q->device_bytes;
+            } else {
+                free_plan(q);
+                cudaGetLastError();
+            }
+        }
+    }
     *plan = p;
     return SPCONV_OK;
 }
@@ -624,6 +645,37 @@ static bool pipe_serves(const Plan *p, int N, uintptr_t x, bool fused, int epi) 
     if (p->kernel != SPCONV_KERNEL_PIPE || (epi && p->pipe_dispatch == 1)) return false;
     spconv::PipeSchedule q;
     return spconv::pipe_schedule(*p, N, x, q, !fused, epi);
+}
+
+// Per call: the R = 2 alternate instead of the R = 4 plan?  A pipe launch takes about
+// max(1, units / SMs) unit times (stream-K spreads a partial round), and an R = 2 unit
+// (half the rows per warp, 12 warps per CTA instead of 8) takes r(density) of an R = 4
+// unit: measured on B200 on the final kernel (profiles/r02/r_crossover_final.jsonl,
+// ab_alt_r2*.jsonl) -- 0.96 at d = 0.05, 0.94 at 0.1, 0.79 at 0.2, 0.67 at 0.3.  c4_80
+// (128 units at R = 4 leave 20 SMs idle; 176 at R = 2): 203.1 -> 190.6 us.
+static double r2_unit_ratio(double d) {
+    static const double xs[] = {0.05, 0.10, 0.20, 0.30, 0.40}, ys[] = {0.96, 0.94, 0.79, 0.67, 0.60};
+    if (d <= xs[0]) return ys[0];
+    for (int i = 1; i < 5; ++i)
+        if (d <= xs[i]) return ys[i - 1] + (ys[i] - ys[i - 1]) * (d - xs[i - 1]) / (xs[i] - xs[i - 1]);
+    return ys[4];
+}
+
+static bool prefer_alt(const Plan *p, int N, uintptr_t x, bool fused, int epi) {
+    if (!p->alt || N <= 0) return false;
+    spconv::PipeSchedule q4, q2;
+    if (!spconv::pipe_schedule(*p, N, x, q4, !fused, epi) || !spconv::pipe_schedule(*p->alt, N, x, q2, !fused, epi))
+        return false;
+    const double sms = double(spconv::sm_count_of_current_device());
+    // a stream-K launch adds a park, a resume and a partial unit per CTA: about 6
+    // channel steps of a unit's C (c2 N=16: R = 2's 168 units on 148 SMs measured 5%
+    // slower than R = 4's 112, while c4_80's 256-channel units gain 6%)
+    auto rounds = [&](const spconv::PipeSchedule &q) {
+        const double r = std::max(1.0, double(q.nunits) / sms);
+        return q.sk ? r * (1.0 + 6.0 / double(p->C)) : r;
+    };
+    const double t4 = rounds(q4), t2 = rounds(q2) * r2_unit_ratio(p->density);
+    return t2 < 0.97 * t4;
 }
 
 static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *argmax, bool fused,
@@ -672,7 +724,8 @@ static int run(spconv_plan_t plan, int N, const float *x, float *y, int32_t *arg
         e = spconv::launch_dense(*p, N, x, y, argmax, fused, s, res, epi);
     else if (pipe_serves(p, N, reinterpret_cast<uintptr_t>(x), fused, epi) &&
              !small_call_prefers_generic(p, N, reinterpret_cast<uintptr_t>(x)))
-        e = spconv::launch_pipe(*p, N, x, y, argmax, fused, s, res, epi);
+        e = spconv::launch_pipe(prefer_alt(p, N, reinterpret_cast<uintptr_t>(x), fused, epi) ? *p->alt : *p, N, x, y,
+                                argmax, fused, s, res, epi);
     else if (p->kernel == SPCONV_KERNEL_TILED && epi == 0)
         e = spconv::launch_tiled(*p, N, x, y, argmax, fused, s);
     else  // the generic kernel serves every epilogue the specialised kernel lacks
@@ -896,6 +949,10 @@ int spconv_launch_info(spconv_plan_t plan, int N, int fused, const float *x, spc
             info->kernel = SPCONV_KERNEL_GENERIC;
             info->rows_per_group = 0;
             return SPCONV_OK;
+        }
+        if (prefer_alt(p, N, reinterpret_cast<uintptr_t>(x), fused != 0, 0)) {
+            p = p->alt; // the call runs the R = 2 alternate
+            info->rows_per_group = p->R;
         }
         spconv::PipeSchedule q;
         if (!spconv::pipe_schedule(*p, N, reinterpret_cast<uintptr_t>(x), q, !fused)) return SPCONV_ERR_UNSUPPORTED;

@@ -193,6 +193,12 @@ struct Plan {
         unsigned seq = 0; // launches on this workspace: the counter slot of launch k is k % kSkSlots
     };
     std::vector<SkSlot> sk_ws;
+    // AUTO plans of the pipe kernel at R = 4 and density >= kAltMinDensity also hold the
+    // same layer at R = 2 (a complete plan of its own): per call, AUTO takes it when its
+    // predicted time is lower -- 1.5x the warps per SM and shorter units, worth it when
+    // the R = 4 units leave SMs idle (spconv_api.cu prefer_alt)
+    Plan *alt = nullptr;
+    double density = 0.0;
     // per-warp stream-K split tables (kernel_pipe.cu sk_split), cached per launch shape
     // (under sk_mu): a table depends on the units (N, geometry), the grid and the epilogue
     std::vector<float> sk_cost; // [gset][warp][C]: walk cost of the warp's group in channel c (tap units)
@@ -246,6 +252,7 @@ constexpr int kSkSlots = 64;         // [ticket, finished] pairs, one per launch
 constexpr size_t kSkFlags = kSkSlots * 8; // byte offset of the flags
 // per-warp split tables travel in the kernel parameters: up to kSkTabCta CTAs and
 // kSkTabGpc warps per CTA (4.5 KB); larger grids use the uniform channel split
+constexpr double kAltMinDensity = 0.08;
 constexpr int kSkTabCta = 160;
 constexpr int kSkTabGpc = 12;
 // walk cost model of the split (units of one tap case, ~125 SM cycles on B200), from

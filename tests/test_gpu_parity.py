@@ -1088,3 +1088,28 @@ def test_split_tables_for_many_batch_sizes_interleaved():
     for N, y in outs:
         assert np.array_equal(bits(y.cpu().numpy()), bits(ref[:N])), N
     layer.close()
+
+
+@pytest.mark.parametrize("name,N,want_R", [("c4_80", 64, 2), ("c2", 32, 4), ("c2", 8, 2), ("c5", 2, 4)])
+def test_auto_per_call_r2_alternate(name, N, want_R, monkeypatch):
+    """AUTO pipe plans at density >= 0.15 also hold the layer at R = 2; per call the one
+    with the lower predicted time runs (units per SM x the measured R = 2 / R = 4 unit-time
+    ratio): c4_80 at its bench batch (128 units at R = 4 leave SMs idle) takes R = 2, the
+    c2 bench launch keeps R = 4.  Either way the bits equal the oracle's."""
+    monkeypatch.delenv("SPCONV_PIPE_R", raising=False)
+    monkeypatch.delenv("SPCONV_NO_ALT", raising=False)
+    cfg = synthgen.CONFIGS[name].with_batch(N)
+    L = synthgen.make_layer(cfg)
+    c = L.csr
+    layer = _layer(cfg, c, None, "auto")
+    x = torch.from_numpy(L.x).cuda()
+    info = layer.launch_info(N, False, x)
+    if info["kernel"] == 3:
+        assert info["rows_per_group"] == want_R, info
+    assert layer.info["rows_per_group"] == 4  # the plan's own R; the alternate is per call
+    y = layer(x).cpu().numpy()
+    assert np.array_equal(bits(y), bits(oracle.conv_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, None)))
+    yf, am = layer.fused_relu_maxpool(x)
+    rf, ra = oracle.fused_f32(L.x, cfg.F, 3, 1, 1, c.rowptr, c.colidx, c.values, None)
+    assert np.array_equal(bits(yf.cpu().numpy()), bits(rf)) and np.array_equal(am.cpu().numpy(), ra)
+    layer.close()
